@@ -1,0 +1,419 @@
+"""Benchmark: InfLLM-V2 sparse-attention prefill tokens/s at 128K (MiniCPM4
+GQA: h_q=32, h_kv=2, d_h=128, B=64, |I|=1+32+63) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 131072] [--impl ours|reference]
+
+A step = one `attend` over one 128K-token sequence (K1 compress -> K2 block
+scoring -> K3 top-k (+ float64 boundary re-rank) -> K4 block-sparse
+attention), synthetic make_qkv inputs resident in HBM (Q alone is 1 GiB >
+L2, so no explicit flush is needed).  N>1: one process per GPU (torchrun),
+each rank serves its own sequence (batch x KV-group sharding, no
+collective; weak scaling); time = max over ranks of the device time.
+
+`--impl reference` times the CPU oracle port (oracle/swattn_oracle.py, a
+float64 numpy restatement of the reference's select_blocks + sparse_forward)
+on a bounded row sample of the same workload, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse-attn prefill tokens/s @128K (MiniCPM4 GQA); speedup vs dense FA"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "tflops": d["bf16_tflops"],
+                "tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured"}
+    return {"hbm_gbs": 6650.0, "tflops": 1590.0, "tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import swattn_oracle as O
+    cfg = O.PAPER
+    n = args.n
+    Q, K, V = O.draw_qkv(n, 32, 2, 128, seed=0)
+    rng = np.random.default_rng(0)
+    R = args.cpu_rows
+    samples = []
+    for step in range(args.warmup + args.steps):
+        rows = np.sort(rng.choice(n, size=R, replace=False))
+        t0 = time.perf_counter()
+        top, _, _ = O.select(Q, K, cfg, "approx", rows=rows)
+        full = np.full((2, n, 63), -1, dtype=np.int64)
+        full[:, rows] = top
+        O.sparse_attention(Q, K, V, full, cfg, rows=rows)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            samples.append(R / dt)
+    v = statistics.median(samples)
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * R / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (make_qkv Philox, bf16-rounded)", "impl": "reference",
+        "config": {"workload": f"attend sparse prefill n={n}, batch 1, paper profile",
+                   "n": n, "rows_per_step": R},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"{R} uniformly sampled query rows of the n={n} sequence "
+                                   "per step (select_blocks approx + sparse_forward rows), "
+                                   "numpy float64 oracle port of the reference"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(n, rows_n=96, seed=0):
+    """The oracle port on a bounded row sample (rank 0, N=1)."""
+    from oracle import swattn_oracle as O
+    cfg = O.PAPER
+    Q, K, V = O.draw_qkv(n, 32, 2, 128, seed=seed)
+    rows = np.sort(np.random.default_rng(seed).choice(n, size=rows_n, replace=False))
+    t0 = time.perf_counter()
+    top, _, _ = O.select(Q, K, cfg, "approx", rows=rows)
+    full = np.full((2, n, 63), -1, dtype=np.int64)
+    full[:, rows] = top
+    O.sparse_attention(Q, K, V, full, cfg, rows=rows)
+    dt = time.perf_counter() - t0
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": rows_n / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{rows_n} uniformly sampled query rows of the n={n} workload "
+                      f"(select_blocks approx + sparse_forward), {dt:.1f} s, numpy float64 "
+                      "oracle port of the reference"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2509_24663_b200 import _lib
+    from paper_2509_24663_b200.core import AttentionConfig, make_qkv
+    from paper_2509_24663_b200.counts import (compress_bytes, dense_total_counts,
+                                              selection_total_counts, sparse_total_counts)
+    from paper_2509_24663_b200.switch import attend
+
+    cfg = AttentionConfig()
+    n = args.n
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    Q, K, V = make_qkv(n, 32, 2, 128, seed=rank, device="cuda")
+    O_ = torch.empty_like(Q)
+    lse = torch.empty((n, 32), dtype=torch.float32, device="cuda")
+    wsb = L.swattn_workspace_bytes(c, n)
+    work = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    taken = _lib.ctypes.c_int32(0)
+
+    def step():
+        _lib.check(L.swattn_attend(c, Q.data_ptr(), K.data_ptr(), V.data_ptr(), n, -1, 0, 2,
+                                   O_.data_ptr(), lse.data_ptr(), _lib.ctypes.byref(taken),
+                                   work.data_ptr(), wsb, sh), "attend")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    tokens_per_s = ws * n / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers (H2D + D2H in the timed region)
+    Qh = Q.cpu().pin_memory()
+    Kh = K.cpu().pin_memory()
+    Vh = V.cpu().pin_memory()
+    Oh = torch.empty(O_.shape, dtype=O_.dtype).pin_memory()
+    lh = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+
+    def e2e_step():
+        qd = Qh.to("cuda", non_blocking=True)
+        kd = Kh.to("cuda", non_blocking=True)
+        vd = Vh.to("cuda", non_blocking=True)
+        res, _ = attend(qd, kd, vd, cfg)
+        Oh.copy_(res.output, non_blocking=True)
+        lh.copy_(res.lse, non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = (Q.numel() + K.numel() + V.numel()) * 2
+    d2h = O_.numel() * 2 + lse.numel() * 4
+
+    # ---- per-stage breakdown (same stream, CUDA events) for the roofline
+    stages = stage_breakdown(L, c, cfg, Q, K, V, n, stream)
+    peaks = _peaks()
+    sp_mac, _ = sparse_total_counts(cfg, n)
+    sel = selection_total_counts(cfg, n, approx=True)
+    dn_mac, _ = dense_total_counts(cfg, n)
+    algo = {"K1_compress": ("hbm", compress_bytes(cfg, n)),
+            "K2_block_scores": ("tensor", 2 * sel["mac"]),
+            "K3_topk": ("hbm", _topk_bytes(cfg, n)),
+            "K4_sparse_attention": ("tensor", 2 * sp_mac)}
+    dom = max(algo, key=lambda k: stages.get(k, 0.0))
+    bound, work_amt = algo[dom]
+    dom_ms = stages[dom]
+    if bound == "hbm":
+        achieved, peak, unit = work_amt / (dom_ms / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"
+    else:
+        achieved, peak, unit = work_amt / (dom_ms / 1e3) / 1e12, peaks["tflops_sustained"], "TFLOP/s"
+    traffic = _traffic(dom)
+    dense = dense_comparator(Q, K, V, cfg, n, stream) if rank == 0 and not args.no_dense else {}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (make_qkv Philox normal(0,1), bf16)",
+            "config": {"workload": f"attend (sparse branch) prefill, n={n} tokens, batch 1 per GPU",
+                       "n": n, "batch_per_gpu": 1, "h_q": 32, "h_kv": 2, "d_h": 128, "B": 64,
+                       "budget_blocks": "1+32+63", "selection_mode": "approx",
+                       "parallelism": f"batch x kv-group sharding, {ws} rank(s), no collective",
+                       "l2": "inputs larger than L2 (Q = 1 GiB), no flush"},
+            "roofline": {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
+                         "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"{peaks['source']} "
+                                        f"({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})"},
+            "stages_ms": stages,
+            "e2e": {"value": ws * n / (e2e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": args.steps * 5,
+            "dense_comparator": dense,
+            "clocks": clk.summary(),
+        }
+        if dense.get("ms"):
+            line["speedup_vs_dense"] = dense["ms"] / ms
+        if not args.no_cpu and ws == 1:
+            line["cpu_baseline"] = cpu_baseline_sample(n, rows_n=args.cpu_rows)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _topk_bytes(cfg, n):
+    m1 = (n - cfg.l_C1) // cfg.s_C1 + 1
+    n_cols = -(-m1 // cfg.s)
+    b = np.arange(n) // cfg.B
+    hi = np.minimum(np.maximum(0, b - cfg.N_local + 1), n_cols)
+    cand = np.maximum(0, hi - cfg.N_init)
+    return int(cfg.h_kv * (cand.sum() * 4 + n * cfg.k_top * 4 + n * 4))
+
+
+def _traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get(kernel)
+    return None
+
+
+def stage_breakdown(L, c, cfg, Q, K, V, n, stream, reps=2):
+    import torch
+    from paper_2509_24663_b200 import _lib
+    sh = stream.cuda_stream
+    m1 = L.swattn_num_pooled(n, cfg.l_C1, cfg.s_C1)
+    m2 = L.swattn_num_pooled(n, cfg.l_C2, cfg.s_C2)
+    n_cols = -(-m1 // cfg.s)
+    ld = (n_cols + 3) // 4 * 4
+    kc1 = torch.empty((m1, 2, 128), dtype=torch.bfloat16, device="cuda")
+    kc2 = torch.empty((m2, 2, 128), dtype=torch.bfloat16, device="cuda")
+    scmp = torch.empty((2, n, ld), dtype=torch.float32, device="cuda")
+    flags = torch.empty((2, n, n_cols // 31 + 1), dtype=torch.int64, device="cuda")
+    topk = torch.empty((2, n, cfg.k_top), dtype=torch.int32, device="cuda")
+    cnt = torch.empty((2, n), dtype=torch.int32, device="cuda")
+    O_ = torch.empty_like(Q)
+    lse = torch.empty((n, 32), dtype=torch.float32, device="cuda")
+    wsb = L.swattn_workspace_bytes(c, n)
+    work = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    calls = {
+        "K1_compress": lambda: L.swattn_compress_keys(c, K.data_ptr(), n, kc1.data_ptr(),
+                                                      kc2.data_ptr(), sh),
+        "K2_block_scores": lambda: L.swattn_block_scores(c, Q.data_ptr(), kc1.data_ptr(),
+                                                         kc2.data_ptr(), n, 2, scmp.data_ptr(),
+                                                         ld, flags.data_ptr(), sh),
+        "K3_topk": lambda: L.swattn_topk_blocks(c, scmp.data_ptr(), ld, n, topk.data_ptr(),
+                                                cnt.data_ptr(), sh),
+        "select_total": lambda: L.swattn_select_blocks(c, Q.data_ptr(), K.data_ptr(), n, 2,
+                                                       topk.data_ptr(), cnt.data_ptr(), None,
+                                                       work.data_ptr(), wsb, sh),
+        "K4_sparse_attention": lambda: L.swattn_sparse_fwd(c, Q.data_ptr(), K.data_ptr(),
+                                                           V.data_ptr(), n, topk.data_ptr(),
+                                                           cnt.data_ptr(), O_.data_ptr(),
+                                                           lse.data_ptr(), sh),
+    }
+    out = {}
+    for name, fn in calls.items():
+        _lib.check(fn(), name)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            _lib.check(fn(), name)
+        b.record(stream)
+        torch.cuda.synchronize()
+        out[name] = a.elapsed_time(b) / reps
+    out["rerank_est"] = max(0.0, out["select_total"] - out["K1_compress"] - out["K2_block_scores"]
+                            - out["K3_topk"])
+    return out
+
+
+def dense_comparator(Q, K, V, cfg, n, stream):
+    """Dense causal GQA flash attention of the same shape (library kernel)."""
+    import torch
+    res = {}
+    try:
+        from flash_attn import flash_attn_func
+        fn = lambda: flash_attn_func(Q[None], K[None], V[None], causal=True)
+        name = "flash_attn 2.8.3 (FA2, sm_100 build)"
+    except Exception:
+        import torch.nn.functional as F
+        q = Q.transpose(0, 1)[None]
+        k = K.transpose(0, 1)[None]
+        v = V.transpose(0, 1)[None]
+        fn = lambda: F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+        name = "torch SDPA"
+    try:
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        reps = 3
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        from paper_2509_24663_b200.counts import dense_total_counts
+        mac, _ = dense_total_counts(cfg, n)
+        res = {"impl": name, "ms": ms, "tflops": 2 * mac / (ms / 1e3) / 1e12}
+    except Exception as e:  # pragma: no cover
+        res = {"impl": name, "error": str(e)[:200]}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=131072)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=48)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

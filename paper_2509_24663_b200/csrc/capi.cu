@@ -1,0 +1,390 @@
+// C-ABI entry points (include/swattn_b200.h): validation, workspace carving
+// and stream-ordered orchestration of the K1..K6 kernels.  No allocation,
+// no host synchronisation.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace swattn {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int32_t cuda_check(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return SWATTN_OK;
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return SWATTN_ECUDA;
+}
+
+// kernels (defined in the other translation units)
+int32_t launch_compress(const swattn_config *, const void *, int64_t, void *, void *, cudaStream_t);
+int32_t launch_scores_simt(const swattn_config *, const void *, const void *, const void *, int64_t,
+                           int32_t, float *, int64_t, uint64_t *, int64_t, cudaStream_t);
+int32_t launch_scores_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
+                         int32_t, float *, int64_t, uint64_t *, int64_t, cudaStream_t);
+int32_t launch_shared_scores(const swattn_config *, const void *, const void *, const void *,
+                             int64_t, int32_t, float *, uint8_t *, float *, cudaStream_t);
+int32_t launch_maxpool(const swattn_config *, const float *, int64_t, float *, int64_t,
+                       cudaStream_t);
+int32_t launch_topk(const swattn_config *, const float *, int64_t, int64_t, int32_t *, int32_t *,
+                    int32_t *, int32_t *, int32_t, const uint64_t *, int64_t, cudaStream_t);
+int32_t launch_rerank(const swattn_config *, const void *, const void *, const void *, int64_t,
+                      int32_t, const float *, int64_t, const int32_t *, const int32_t *, int32_t,
+                      int32_t *, int, cudaStream_t);
+int32_t launch_attention_simt(const swattn_config *, const void *, const void *, const void *,
+                              int64_t, const int32_t *, const int32_t *, int, int, void *, float *,
+                              int *, cudaStream_t);
+int32_t launch_sparse_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
+                         const int32_t *, const int32_t *, void *, float *, cudaStream_t);
+int32_t launch_dense_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
+                        int, void *, float *, cudaStream_t);
+bool scores_tc_available();
+bool attention_tc_available();
+
+static int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct SelectLayout {
+  int64_t m1, m2, n_cols, ld, ld_f;
+  size_t off_kc1, off_kc2, off_scmp, off_flags, off_count, off_rows, off_shared, off_lse, total;
+  bool generic;
+};
+
+static SelectLayout select_layout(const swattn_config *cfg, int64_t n) {
+  SelectLayout L{};
+  L.m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
+  L.m2 = num_pooled(n, cfg->l_C2, cfg->s_C2);
+  L.n_cols = L.m1 ? cdiv(L.m1, cfg->s) : 0;
+  L.ld = ((L.n_cols + 3) / 4) * 4;
+  if (L.ld == 0) L.ld = 4;
+  L.ld_f = L.n_cols / 31 + 1;
+  L.generic = swattn_profile_supported(cfg) == 0;
+  size_t o = 0;
+  L.off_kc1 = o; o = align_up(o + (size_t)L.m1 * cfg->h_kv * cfg->d_h * 2);
+  L.off_kc2 = o; o = align_up(o + (size_t)L.m2 * cfg->h_kv * cfg->d_h * 2);
+  L.off_scmp = o; o = align_up(o + (size_t)cfg->h_kv * n * L.ld * 4);
+  L.off_flags = o; o = align_up(o + (size_t)cfg->h_kv * n * L.ld_f * 8);
+  L.off_count = o; o = align_up(o + 16);
+  L.off_rows = o; o = align_up(o + (size_t)cfg->h_kv * n * 4);
+  L.off_shared = o;
+  if (L.generic) o = align_up(o + (size_t)n * cfg->h_kv * L.m1 * 4);
+  L.off_lse = o;
+  if (L.generic) o = align_up(o + (size_t)n * cfg->h_q * 4);
+  L.total = o;
+  return L;
+}
+
+static int32_t check_ptr(const void *p, const char *name) {
+  if (p == nullptr) {
+    set_error("%s must not be NULL", name);
+    return SWATTN_EINVAL;
+  }
+  return SWATTN_OK;
+}
+
+}  // namespace swattn
+
+using namespace swattn;
+
+extern "C" {
+
+const char *swattn_last_error(void) { return g_err; }
+
+int32_t swattn_version(void) { return 1000; }
+
+int32_t swattn_validate_config(const swattn_config *cfg) {
+  if (cfg == nullptr) {
+    set_error("config must not be NULL");
+    return SWATTN_EINVAL;
+  }
+  // core.py:118-135, in the reference's field order
+  const struct { const char *name; int32_t v; } pos[] = {
+      {"h_q", cfg->h_q},       {"h_kv", cfg->h_kv},       {"d_h", cfg->d_h},
+      {"B", cfg->B},           {"l_C1", cfg->l_C1},       {"s_C1", cfg->s_C1},
+      {"l_C2", cfg->l_C2},     {"s_C2", cfg->s_C2},       {"l", cfg->l},
+      {"s", cfg->s},           {"N_init", cfg->N_init},   {"N_local", cfg->N_local},
+      {"w", cfg->w}};
+  for (const auto &p : pos) {
+    if (p.v < 1) {
+      set_error("positivity: %s=%d must be a positive integer", p.name, p.v);
+      return SWATTN_EINVAL;
+    }
+  }
+  if (cfg->k_top < 0) {
+    set_error("positivity: k_top=%d must be >= 0", cfg->k_top);
+    return SWATTN_EINVAL;
+  }
+  if (cfg->h_q % cfg->h_kv != 0) {  // core.py:143-146
+    set_error("head-divisibility: h_q=%d is not a multiple of h_kv=%d", cfg->h_q, cfg->h_kv);
+    return SWATTN_EINVAL;
+  }
+  if (!cfg->experimental) {  // core.py:152-168
+    if (cfg->s_C1 > cfg->l_C1) {
+      set_error("pooling-profile: stride s_C1=%d exceeds window l_C1=%d", cfg->s_C1, cfg->l_C1);
+      return SWATTN_EINVAL;
+    }
+    if (cfg->s_C2 > cfg->l_C2) {
+      set_error("pooling-profile: stride s_C2=%d exceeds window l_C2=%d", cfg->s_C2, cfg->l_C2);
+      return SWATTN_EINVAL;
+    }
+    if (cfg->l_C1 % cfg->s_C1 != 0) {
+      set_error("pooling-profile: s_C1=%d must divide l_C1=%d", cfg->s_C1, cfg->l_C1);
+      return SWATTN_EINVAL;
+    }
+    if ((cfg->l - 1) % cfg->s != 0) {
+      set_error("pooling-profile: s=%d must divide l-1=%d", cfg->s, cfg->l - 1);
+      return SWATTN_EINVAL;
+    }
+  }
+  const int32_t needed = (cfg->w + cfg->B - 1) / cfg->B + 1;  // core.py:170-175
+  if (cfg->N_local < needed) {
+    set_error("window-coverage: N_local=%d < ceil(w/B)+1=%d (w=%d, B=%d)", cfg->N_local, needed,
+              cfg->w, cfg->B);
+    return SWATTN_EINVAL;
+  }
+  return SWATTN_OK;
+}
+
+int32_t swattn_profile_supported(const swattn_config *cfg) {
+  if (cfg == nullptr) return 0;
+  return cfg->h_q == kG * cfg->h_kv && cfg->d_h == kD && cfg->B == kB && cfg->l == kPoolL &&
+         cfg->s == kPoolS && cfg->l_C1 == 2 * cfg->s_C1 && cfg->s_C2 == 4 * cfg->s_C1 &&
+         cfg->l_C2 == 2 * cfg->s_C2 && kPoolS * cfg->s_C1 == cfg->B && cfg->k_top <= kTopMax &&
+         cfg->N_init + cfg->N_local <= 64;
+}
+
+int64_t swattn_num_pooled(int64_t n, int32_t length, int32_t stride) {
+  return num_pooled(n, length, stride);
+}
+
+size_t swattn_workspace_bytes(const swattn_config *cfg, int64_t n) {
+  if (cfg == nullptr || n < 1) return 0;
+  const SelectLayout L = select_layout(cfg, n);
+  // attend additionally keeps the top-k lists
+  return align_up(L.total) + align_up((size_t)cfg->h_kv * n * cfg->k_top * 4) +
+         align_up((size_t)cfg->h_kv * n * 4) + 256;
+}
+
+int32_t swattn_compress_keys(const swattn_config *cfg, const void *K, int64_t n, void *kc1,
+                             void *kc2, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  if ((rc = check_ptr(K, "K"))) return rc;
+  if (num_pooled(n, cfg->l_C1, cfg->s_C1) > 0 && (rc = check_ptr(kc1, "kc1"))) return rc;
+  return launch_compress(cfg, K, n, kc1, kc2, static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_block_scores(const swattn_config *cfg, const void *Q, const void *kc1,
+                            const void *kc2, int64_t n, int32_t mode, float *s_cmp, int64_t ld,
+                            uint64_t *flags, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (!swattn_profile_supported(cfg)) {
+    set_error("unsupported profile for the fused block-scoring kernel (need G=16, d_h=128, B=64, "
+              "l=5, s=4, l_C1=2*s_C1, s_C2=4*s_C1, l_C2=2*s_C2)");
+    return SWATTN_EUNSUPPORTED;
+  }
+  if (mode < 0 || mode > 2) {
+    set_error("unknown selection mode %d", mode);
+    return SWATTN_EINVAL;
+  }
+  const SelectLayout L = select_layout(cfg, n);
+  if (ld < L.n_cols) {
+    set_error("ld=%lld is smaller than the %lld block-score columns", (long long)ld,
+              (long long)L.n_cols);
+    return SWATTN_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (scores_tc_available())
+    return launch_scores_tc(cfg, Q, kc1, kc2, n, mode, s_cmp, ld, flags, L.ld_f, st);
+  return launch_scores_simt(cfg, Q, kc1, kc2, n, mode, s_cmp, ld, flags, L.ld_f, st);
+}
+
+int32_t swattn_shared_scores(const swattn_config *cfg, const void *Q, const void *kc1,
+                             const void *kc2, int64_t n, int32_t mode, float *shared,
+                             uint8_t *no_visible, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (cfg->d_h > 256) {
+    set_error("unsupported: d_h=%d > 256 in the debug scoring path", cfg->d_h);
+    return SWATTN_EUNSUPPORTED;
+  }
+  // lse scratch lives at the tail of the caller's shared buffer contract:
+  // allocate it from the stream-ordered pool (debug path only).
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float *lse = nullptr;
+  if (cudaMallocAsync(&lse, (size_t)n * cfg->h_q * sizeof(float), st) != cudaSuccess)
+    return cuda_check(cudaGetLastError(), "cudaMallocAsync(lse)");
+  rc = launch_shared_scores(cfg, Q, kc1, kc2, n, mode, shared, no_visible, lse, st);
+  cudaFreeAsync(lse, st);
+  return rc;
+}
+
+int32_t swattn_topk_blocks(const swattn_config *cfg, const float *s_cmp, int64_t ld, int64_t n,
+                           int32_t *topk, int32_t *topk_cnt, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  return launch_topk(cfg, s_cmp, ld, n, topk, topk_cnt, nullptr, nullptr, 0, nullptr, 0,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void *K, int64_t n,
+                             int32_t mode, int32_t *topk, int32_t *topk_cnt, int32_t *n_reranked,
+                             void *workspace, size_t workspace_bytes, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  if (mode < 0 || mode > 2) {
+    set_error("unknown selection mode %d", mode);
+    return SWATTN_EINVAL;
+  }
+  const SelectLayout L = select_layout(cfg, n);
+  if (workspace_bytes < L.total || workspace == nullptr) {
+    set_error("workspace too small: %zu < %zu bytes", workspace_bytes, L.total);
+    return SWATTN_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *ws = static_cast<char *>(workspace);
+  void *kc1 = ws + L.off_kc1;
+  void *kc2 = ws + L.off_kc2;
+  float *scmp = reinterpret_cast<float *>(ws + L.off_scmp);
+  uint64_t *flags = reinterpret_cast<uint64_t *>(ws + L.off_flags);
+  int32_t *count = reinterpret_cast<int32_t *>(ws + L.off_count);
+  int32_t *rows = reinterpret_cast<int32_t *>(ws + L.off_rows);
+  if ((rc = launch_compress(cfg, K, n, kc1, kc2, st))) return rc;
+  if (cfg->k_top == 0 || L.n_cols <= cfg->N_init) {
+    if (cfg->k_top > 0) {
+      // no row has candidates: all-empty top-k lists
+      if ((rc = cuda_check(cudaMemsetAsync(topk, 0xff, (size_t)cfg->h_kv * n * cfg->k_top * 4, st),
+                           "memset(topk)")))
+        return rc;
+    }
+    if ((rc = cuda_check(cudaMemsetAsync(topk_cnt, 0, (size_t)cfg->h_kv * n * 4, st), "memset")))
+      return rc;
+    if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
+    return SWATTN_OK;
+  }
+  if (L.generic) {
+    // any-profile path: full S^shared, max-pool, top-k (no float64 boundary pass)
+    float *shared = reinterpret_cast<float *>(ws + L.off_shared);
+    float *lse = reinterpret_cast<float *>(ws + L.off_lse);
+    if ((rc = launch_shared_scores(cfg, Q, kc1, kc2, n, mode, shared, nullptr, lse, st))) return rc;
+    if ((rc = launch_maxpool(cfg, shared, n, scmp, L.ld, st))) return rc;
+    rc = launch_topk(cfg, scmp, L.ld, n, topk, topk_cnt, nullptr, nullptr, 0, nullptr, 0, st);
+    if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
+    return rc;
+  }
+  if (scores_tc_available())
+    rc = launch_scores_tc(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
+  else
+    rc = launch_scores_simt(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
+  if (rc) return rc;
+  if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset(count)"))) return rc;
+  const int32_t cap = (int32_t)((int64_t)cfg->h_kv * n);
+  if ((rc = launch_topk(cfg, scmp, L.ld, n, topk, topk_cnt, count, rows, cap, flags, L.ld_f, st)))
+    return rc;
+  if ((rc = launch_rerank(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, count, rows, cap, topk, num_sms(),
+                          st)))
+    return rc;
+  if (n_reranked)
+    return cuda_check(cudaMemcpyAsync(n_reranked, count, 4, cudaMemcpyDeviceToDevice, st),
+                      "copy(n_reranked)");
+  return SWATTN_OK;
+}
+
+int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                          int64_t n, const int32_t *topk, const int32_t *topk_cnt, void *O,
+                          float *lse, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  if (cfg->h_q != kG * cfg->h_kv || cfg->d_h != kD) {
+    set_error("unsupported profile for the attention kernels (need G=16, d_h=128)");
+    return SWATTN_EUNSUPPORTED;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (attention_tc_available() && swattn_profile_supported(cfg))
+    return launch_sparse_tc(cfg, Q, K, V, n, topk, topk_cnt, O, lse, st);
+  return launch_attention_simt(cfg, Q, K, V, n, topk, topk_cnt, 1, 1, O, lse, nullptr, st);
+}
+
+int32_t swattn_dense_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                         int64_t n, int32_t causal, void *O, float *lse, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  if (cfg->h_q != kG * cfg->h_kv || cfg->d_h != kD) {
+    set_error("unsupported profile for the attention kernels (need G=16, d_h=128)");
+    return SWATTN_EUNSUPPORTED;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (attention_tc_available())
+    return launch_dense_tc(cfg, Q, K, V, n, causal, O, lse, st);
+  return launch_attention_simt(cfg, Q, K, V, n, nullptr, nullptr, 0, causal, O, lse, nullptr, st);
+}
+
+int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                      int64_t n, int64_t threshold, int32_t forced_mode, int32_t select_mode,
+                      void *O, float *lse, int32_t *mode_taken, void *workspace,
+                      size_t workspace_bytes, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (forced_mode < 0 || forced_mode > 2) {
+    set_error("unknown forced mode %d", forced_mode);
+    return SWATTN_EINVAL;
+  }
+  // switch.py:63-69
+  const int64_t thr =
+      threshold >= 0 ? threshold : (int64_t)(cfg->N_init + cfg->N_local + cfg->k_top) * cfg->B;
+  const bool dense = forced_mode == SWATTN_FORCE_DENSE || (forced_mode == SWATTN_AUTO && n <= thr);
+  if (mode_taken) *mode_taken = dense ? 1 : 2;
+  if (dense) return swattn_dense_fwd(cfg, Q, K, V, n, 1, O, lse, stream);
+  const SelectLayout L = select_layout(cfg, n);
+  const size_t need = swattn_workspace_bytes(cfg, n);
+  if (workspace == nullptr || workspace_bytes < need) {
+    set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
+    return SWATTN_EINVAL;
+  }
+  char *ws = static_cast<char *>(workspace);
+  int32_t *topk = reinterpret_cast<int32_t *>(ws + align_up(L.total));
+  int32_t *cnt = reinterpret_cast<int32_t *>(ws + align_up(L.total) +
+                                             align_up((size_t)cfg->h_kv * n * cfg->k_top * 4));
+  if ((rc = swattn_select_blocks(cfg, Q, K, n, select_mode, topk, cnt, nullptr, workspace, L.total,
+                                 stream)))
+    return rc;
+  return swattn_sparse_fwd(cfg, Q, K, V, n, topk, cnt, O, lse, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,243 @@
+// Float64 boundary re-rank for selection exactness.
+//
+// K2 produces S^cmp in float32 with a bounded relative error (kScoreRelErr).
+// K3 flags rows whose k-th / (k+1)-th boundary lies inside that bound; this
+// kernel recomputes, for each flagged row, the pass-1 log-sum-exp of all 16
+// heads and the max-pooled scores of the boundary cluster in float64 -- the
+// reference's own arithmetic (selection.py:165-222, :336-348,
+// compression.py:160-173) -- and settles the cluster with the reference's
+// ordering (score desc, index asc; selection.py:125).  Blocks clearly above
+// the cluster stay selected, blocks clearly below stay out.
+#include "common.cuh"
+
+namespace swattn {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxCluster = 256;
+
+struct RerankArgs {
+  const __nv_bfloat16 *Q, *kc1, *kc2;
+  const float *s_cmp;
+  int64_t ld, n, m1, m2;
+  int h_kv, h_q, B, N_init, N_local, k_top, n_cols;
+  int l_C1, s_C1, l_C2, s_C2, pl, ps;
+  int approx;
+  double scale;
+  const int32_t *count;
+  const int32_t *rows;
+  int cap;
+  int32_t *topk;
+};
+
+__device__ double block_reduce_max(double v, double *red) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = -INFINITY;
+  for (int w = 0; w < kThreads / 32; ++w) v = fmax(v, red[w]);
+  return v;
+}
+__device__ double block_reduce_sum(double v, double *red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = 0.0;
+  for (int w = 0; w < kThreads / 32; ++w) v += red[w];
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
+  __shared__ double q_s[kG][kD];
+  __shared__ double lse_s[kG];
+  __shared__ double red[kThreads / 32];
+  __shared__ int members[kMaxCluster];
+  __shared__ double mscore[kMaxCluster];
+  __shared__ int n_members, n_above;
+  __shared__ int out_s[kTopMax];
+
+  const int total = min(*a.count, a.cap);
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int row = a.rows[item];
+    const int g = row / (int)a.n;
+    const int64_t i = row % a.n;
+    const int b = (int)(i / a.B);
+    const int hi = cand_hi(b, a.N_local, a.n_cols);
+    const int ncand = hi - a.N_init;
+    const int k = min(a.k_top, ncand);
+    for (int t = threadIdx.x; t < kG * kD; t += kThreads) {
+      const int h = t / kD, d = t % kD;
+      q_s[h][d] = (double)bf2f(a.Q[(i * a.h_q + g * kG + h) * kD + d]);
+    }
+    __syncthreads();
+
+    // ---- pass 1 in float64: lse over the visible normaliser columns
+    const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
+    const int64_t vis2 = a.approx ? vis_count(i, a.l_C2, a.s_C2) : 0;
+    const bool use_c2 = a.approx && vis2 > 0;
+    const __nv_bfloat16 *kc = use_c2 ? a.kc2 : a.kc1;
+    const int64_t vis = use_c2 ? vis2 : vis1;
+    double mloc[kG], lloc[kG];
+#pragma unroll
+    for (int h = 0; h < kG; ++h) { mloc[h] = -INFINITY; lloc[h] = 0.0; }
+    for (int64_t c = threadIdx.x; c < vis; c += kThreads) {
+      double acc[kG];
+#pragma unroll
+      for (int h = 0; h < kG; ++h) acc[h] = 0.0;
+      const __nv_bfloat16 *kr = kc + (c * a.h_kv + g) * kD;
+      for (int d = 0; d < kD; d += 8) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4 *>(kr + d));
+        const __nv_bfloat16 *kv = reinterpret_cast<const __nv_bfloat16 *>(&raw);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double kd = (double)bf2f(kv[e]);
+#pragma unroll
+          for (int h = 0; h < kG; ++h) acc[h] = fma(q_s[h][d + e], kd, acc[h]);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < kG; ++h) {
+        const double s = acc[h] * a.scale;
+        if (s > mloc[h]) { lloc[h] = lloc[h] * exp(mloc[h] - s) + 1.0; mloc[h] = s; }
+        else lloc[h] += exp(s - mloc[h]);
+      }
+    }
+    for (int h = 0; h < kG; ++h) {
+      const double M = block_reduce_max(mloc[h], red);
+      const double part = (mloc[h] == -INFINITY) ? 0.0 : lloc[h] * exp(mloc[h] - M);
+      const double L = block_reduce_sum(part, red);
+      if (threadIdx.x == 0) lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe
+    }
+
+    // ---- the boundary cluster from the float32 scores
+    const float *src = a.s_cmp + (int64_t)row * a.ld;
+    // k-th largest float32 score (same order as K3)
+    uint32_t T = 0;
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t candk = T | (1u << bit);
+      int c = 0;
+      for (int t = threadIdx.x; t < ncand; t += kThreads) c += f2key(src[a.N_init + t]) >= candk;
+      c = (int)block_reduce_sum((double)c, red);
+      if (c >= k) T = candk;
+    }
+    const float vk = key2f(T);
+    const float band = 3.0f * kScoreRelErr * fabsf(vk);
+    if (threadIdx.x == 0) { n_members = 0; n_above = 0; }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ncand; t += kThreads) {
+      const float v = src[a.N_init + t];
+      if (v > vk + band) atomicAdd(&n_above, 1);
+      else if (v >= vk - band) {
+        const int slot = atomicAdd(&n_members, 1);
+        if (slot < kMaxCluster) members[slot] = a.N_init + t;
+      }
+    }
+    __syncthreads();
+    const int nm = min(n_members, kMaxCluster);
+
+    // ---- float64 max-pooled scores of the cluster members
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int mi = warp; mi < nm; mi += kThreads / 32) {
+      const int j = members[mi];
+      double best = -INFINITY;
+      for (int e = 0; e < a.pl; ++e) {
+        const int64_t c = (int64_t)j * a.ps + e;
+        if (c >= a.m1) break;
+        double sh = 0.0;
+        if (c < vis1) {
+          const __nv_bfloat16 *kr = a.kc1 + (c * a.h_kv + g) * kD;
+          for (int h = 0; h < kG; ++h) {
+            double dot = 0.0;
+            for (int d = lane; d < kD; d += 32) dot = fma(q_s[h][d], (double)bf2f(kr[d]), dot);
+            for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            sh += exp(dot * a.scale - lse_s[h]);
+          }
+        }
+        best = fmax(best, sh);
+      }
+      if (lane == 0) mscore[mi] = best;
+    }
+    __syncthreads();
+
+    // ---- settle: slots = k - above; rank members by (score desc, index asc)
+    if (threadIdx.x == 0) {
+      const int slots = k - n_above;
+      // selection sort over the (small) cluster
+      int chosen = 0;
+      for (int s = 0; s < slots && s < nm; ++s) {
+        int best = -1;
+        for (int mi = 0; mi < nm; ++mi) {
+          if (members[mi] < 0) continue;
+          if (best < 0 || mscore[mi] > mscore[best] ||
+              (mscore[mi] == mscore[best] && members[mi] < members[best]))
+            best = mi;
+        }
+        out_s[chosen++] = members[best];
+        members[best] = -1 - members[best];  // mark taken (keeps value recoverable)
+      }
+      // merge: above-cluster blocks + chosen, ascending
+      int w = 0;
+      int32_t *out = a.topk + (int64_t)row * a.k_top;
+      int ci = 0;
+      // sort chosen ascending (tiny)
+      for (int x = 1; x < chosen; ++x) {
+        int v = out_s[x], y = x - 1;
+        while (y >= 0 && out_s[y] > v) { out_s[y + 1] = out_s[y]; --y; }
+        out_s[y + 1] = v;
+      }
+      for (int t = 0; t < ncand; ++t) {
+        const int j = a.N_init + t;
+        const bool above = src[j] > vk + band;
+        while (ci < chosen && out_s[ci] < j) out[w++] = out_s[ci++];
+        if (above) out[w++] = j;
+      }
+      while (ci < chosen) out[w++] = out_s[ci++];
+      for (; w < a.k_top; ++w) out[w] = -1;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int32_t launch_rerank(const swattn_config *cfg, const void *Q, const void *kc1, const void *kc2,
+                      int64_t n, int32_t mode, const float *s_cmp, int64_t ld,
+                      const int32_t *count, const int32_t *rows, int32_t cap, int32_t *topk,
+                      int num_sms, cudaStream_t stream) {
+  if (cfg->k_top > kTopMax) {
+    set_error("unsupported: k_top=%d exceeds the compiled bound %d", cfg->k_top, kTopMax);
+    return SWATTN_EUNSUPPORTED;
+  }
+  RerankArgs a;
+  a.Q = static_cast<const __nv_bfloat16 *>(Q);
+  a.kc1 = static_cast<const __nv_bfloat16 *>(kc1);
+  a.kc2 = static_cast<const __nv_bfloat16 *>(kc2);
+  a.s_cmp = s_cmp;
+  a.ld = ld;
+  a.n = n;
+  a.m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
+  a.m2 = num_pooled(n, cfg->l_C2, cfg->s_C2);
+  a.h_kv = cfg->h_kv;
+  a.h_q = cfg->h_q;
+  a.B = cfg->B;
+  a.N_init = cfg->N_init;
+  a.N_local = cfg->N_local;
+  a.k_top = cfg->k_top;
+  a.n_cols = (int)(a.m1 ? cdiv(a.m1, cfg->s) : 0);
+  a.l_C1 = cfg->l_C1; a.s_C1 = cfg->s_C1; a.l_C2 = cfg->l_C2; a.s_C2 = cfg->s_C2;
+  a.pl = cfg->l; a.ps = cfg->s;
+  a.approx = mode == SWATTN_SELECT_APPROX;
+  a.scale = cfg->scale_compressed_logits ? 1.0 / sqrt((double)cfg->d_h) : 1.0;
+  a.count = count;
+  a.rows = rows;
+  a.cap = cap;
+  a.topk = topk;
+  rerank_kernel<<<num_sms * 2, kThreads, 0, stream>>>(a);
+  SWATTN_LAUNCH_CHECK("rerank_kernel");
+  return SWATTN_OK;
+}
+
+}  // namespace swattn

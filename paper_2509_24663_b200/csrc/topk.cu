@@ -1,0 +1,166 @@
+// K3 -- per-row top-k block selection (build_block_sets, selection.py:93-136).
+//
+// One warp per (group, query row).  The candidate pool of row i in query
+// block b is [N_init, min(b - N_local + 1, n_cols)); k = min(k_top, #cand)
+// (0 for rows with no visible pooled entry, :129).  Ranking is score
+// descending with ties to the lower block index -- exactly the stable
+// argsort of :125 -- realised as a radix select on the order-preserving
+// uint32 image of the fp32 score followed by an index-ordered compaction
+// (so the output is already ascending, like np.unique at :133).
+//
+// When `amb` is given (select path), rows whose k-th / (k+1)-th boundary is
+// within the float32 error bound of S^cmp are appended to a list for the
+// float64 re-rank (rerank.cu); exact structural ties (adjacent blocks whose
+// max-pool windows share the argmax column, see scores.cu flags) are not
+// ambiguous and resolve by index exactly as in float64.
+//
+// Roofline: HBM-bound; bytes = candidate S^cmp fp32 read + topk int32 write.
+#include "common.cuh"
+
+namespace swattn {
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kMaxCand = 4096;  // per-row candidate bound held in smem
+
+struct AmbList {
+  int32_t *count;      // device counter
+  int32_t *rows;       // [cap] packed (g * n + i)
+  int32_t cap;
+  const uint64_t *flags;  // [h_kv, n, ld_f] or null
+  int64_t ld_f;
+};
+
+__device__ __forceinline__ int warp_count(bool p) { return __popc(__ballot_sync(0xffffffffu, p)); }
+
+__global__ void __launch_bounds__(kWarps * 32)
+topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, int B,
+            int N_init, int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
+            int32_t *__restrict__ topk,
+            int32_t *__restrict__ topk_cnt, AmbList amb) {
+  extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;  // g * n + i
+  if (row >= (int64_t)h_kv * n) return;
+  const int64_t i = row % n;
+  const int b = (int)(i / B);
+  const int hi = cand_hi(b, N_local, n_cols);
+  const int ncand = hi > N_init ? hi - N_init : 0;
+  const bool no_visible = (i + 1) < l_C1;
+  const int k = no_visible ? 0 : (ncand < k_top ? ncand : k_top);
+  int32_t *out = topk + row * k_top;
+  if (lane == 0) topk_cnt[row] = k;
+
+  if (k == ncand) {  // every candidate is selected (or none)
+    for (int t = lane; t < k_top; t += 32) out[t] = t < k ? N_init + t : -1;
+    return;
+  }
+  const float *src = s_cmp + row * ld + N_init;
+  uint32_t *ks = keys_s + (size_t)warp * cand_stride;
+  for (int t = lane; t < ncand; t += 32) ks[t] = f2key(src[t]);
+  __syncwarp();
+
+  // largest T with #(key >= T) >= k  ==  the k-th largest key
+  uint32_t T = 0;
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t cand = T | (1u << bit);
+    int c = 0;
+    for (int t = lane; t < ncand; t += 32) c += ks[t] >= cand;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (c >= k) T = cand;
+  }
+  int gt = 0, eq = 0;
+  uint32_t below = 0;  // largest key < T
+  for (int t = lane; t < ncand; t += 32) {
+    const uint32_t v = ks[t];
+    gt += v > T;
+    eq += v == T;
+    if (v < T && v > below) below = v;
+  }
+  gt = __reduce_add_sync(0xffffffffu, gt);
+  eq = __reduce_add_sync(0xffffffffu, eq);
+  below = __reduce_max_sync(0xffffffffu, below);
+  const int need_eq = k - gt;
+
+  // index-ordered compaction: key > T, or key == T among the first need_eq
+  int written = 0, eq_seen = 0;
+  for (int base = 0; base < ncand; base += 32) {
+    const int t = base + lane;
+    const uint32_t v = t < ncand ? ks[t] : 0u;
+    const bool is_eq = t < ncand && v == T;
+    const unsigned eq_mask = __ballot_sync(0xffffffffu, is_eq);
+    const int eq_rank = eq_seen + __popc(eq_mask & ((1u << lane) - 1u));
+    const bool take = t < ncand && (v > T || (is_eq && eq_rank < need_eq));
+    const unsigned take_mask = __ballot_sync(0xffffffffu, take);
+    if (take) out[written + __popc(take_mask & ((1u << lane) - 1u))] = N_init + t;
+    written += __popc(take_mask);
+    eq_seen += __popc(eq_mask);
+  }
+  for (int t = written + lane; t < k_top; t += 32) out[t] = -1;
+
+  if (amb.count == nullptr) return;
+  // ---- ambiguity of the k / k+1 boundary under the float32 error bound
+  const float vk = key2f(T);
+  bool ambiguous;
+  if (gt + eq > k) {
+    // an exact float32 tie straddles the boundary: safe only if it is the
+    // structural tie of two adjacent blocks whose max-pool windows both take
+    // their maximum from the shared column (flags R_j and L_{j+1}).
+    ambiguous = true;
+    if (eq == 2 && amb.flags != nullptr) {
+      int first = -1, second = -1;
+      for (int base = 0; base < ncand; base += 32) {
+        const int t = base + lane;
+        unsigned mm = __ballot_sync(0xffffffffu, t < ncand && ks[t] == T);
+        while (mm) {
+          const int pos = base + __ffs(mm) - 1;
+          mm &= mm - 1;
+          if (first < 0) first = pos; else if (second < 0) second = pos;
+        }
+      }
+      if (second == first + 1) {
+        const int j = N_init + first;  // global block index
+        const uint64_t *fr = amb.flags + row * amb.ld_f;
+        const int tj = j / 31, qj = j % 31, tj1 = (j + 1) / 31, qj1 = (j + 1) % 31;
+        const bool R_j = (fr[tj] >> (2 * qj + 1)) & 1ull;
+        const bool L_j1 = (fr[tj1] >> (2 * qj1)) & 1ull;
+        ambiguous = !(R_j && L_j1);
+      }
+    }
+  } else {
+    const float vb = below ? key2f(below) : -INFINITY;
+    ambiguous = (vk - vb) <= 3.0f * kScoreRelErr * fabsf(vk);
+  }
+  if (ambiguous && lane == 0) {
+    const int slot = atomicAdd(amb.count, 1);
+    if (slot < amb.cap) amb.rows[slot] = (int32_t)row;
+  }
+}
+
+}  // namespace
+
+int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, int64_t n,
+                    int32_t *topk, int32_t *topk_cnt, int32_t *amb_count, int32_t *amb_rows,
+                    int32_t amb_cap, const uint64_t *flags, int64_t ld_f, cudaStream_t stream) {
+  const int64_t m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
+  const int n_cols = (int)(m1 ? cdiv(m1, cfg->s) : 0);
+  if (n_cols - cfg->N_init > kMaxCand) {
+    set_error("unsupported: %d top-k candidates exceed the compiled bound %d", n_cols, kMaxCand);
+    return SWATTN_EUNSUPPORTED;
+  }
+  if (cfg->k_top <= 0) return SWATTN_OK;
+  const int64_t rows = (int64_t)cfg->h_kv * n;
+  AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
+  const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
+  const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  topk_kernel<<<(unsigned)cdiv(rows, kWarps), kWarps * 32, smem, stream>>>(
+      s_cmp, ld, n, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols, cfg->l_C1,
+      cand_stride, topk, topk_cnt, amb);
+  SWATTN_LAUNCH_CHECK("topk_kernel");
+  return SWATTN_OK;
+}
+
+}  // namespace swattn

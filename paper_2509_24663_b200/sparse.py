@@ -1,0 +1,61 @@
+"""Block-sparse attention over the selected blocks (reference: sparse.py) -- K4."""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._tensors import is_host, to_device_bf16
+from .core import AttentionConfig, OpCounter
+from .dense import AttentionResult, _finish, check_gqa_shapes
+from .selection import BlockSelection
+
+
+def _check_selection(sel: BlockSelection, n: int, h_kv: int) -> None:
+    """sparse.py:26-30."""
+    if sel.n != n:
+        raise ValueError(f"selection built for n={sel.n}, inputs have n={n}")
+    if sel.num_groups != h_kv:
+        raise ValueError(f"selection has {sel.num_groups} groups, inputs have h_kv={h_kv}")
+
+
+def sparse_forward(Q, K, V, sel: BlockSelection, cfg: AttentionConfig,
+                   counter: OpCounter | None = None, stats: dict | None = None) -> AttentionResult:
+    """sparse.py:43-98 on the GPU: exact online softmax over each token's
+    init U local U top-k blocks, diagonal block causally clipped."""
+    n, h_q, h_kv, d_h = check_gqa_shapes(Q, K, V, cfg)
+    _check_selection(sel, n, h_kv)
+    host = is_host(Q)
+    Qd, Kd, Vd = (to_device_bf16(x, nm) for x, nm in ((Q, "Q"), (K, "K"), (V, "V")))
+    O = torch.empty((n, h_q, d_h), dtype=torch.bfloat16, device=Qd.device)
+    lse = torch.empty((n, h_q), dtype=torch.float32, device=Qd.device)
+    topk = sel.topk.contiguous()
+    if topk.shape[2] != cfg.k_top:
+        raise ValueError(f"selection k_top={topk.shape[2]} != cfg.k_top={cfg.k_top}")
+    L = _lib.lib()
+    _lib.check(L.swattn_sparse_fwd(_lib.c_config(cfg), Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(),
+                                   n, topk.data_ptr(), sel.topk_cnt.data_ptr(), O.data_ptr(),
+                                   lse.data_ptr(), _lib.stream_handle(Qd.device)),
+               "swattn_sparse_fwd")
+    if counter is not None or stats is not None:
+        cnt = sel.topk_cnt.to(torch.int64)
+        i = torch.arange(n, device=cnt.device)
+        b = i // cfg.B
+        picked = torch.clamp(b + 1, max=cfg.N_init + cfg.N_local) + cnt  # per (g, i)
+        visits = (picked - 1) * cfg.B + (i - b * cfg.B) + 1
+        if counter is not None:
+            total = int(visits.sum())
+            counter.add(mac=2 * total * (h_q // h_kv) * d_h, exp=total * (h_q // h_kv))
+        if stats is not None:
+            stats["key_visits"] = visits.cpu().numpy()
+    return _finish(O, lse, host)
+
+
+def token_visibility_mask(sel: BlockSelection, g: int):
+    """sparse.py:33-40 (host bool [n, n]; small n only)."""
+    import numpy as np
+    mask = np.zeros((sel.n, sel.n), dtype=bool)
+    for i in range(sel.n):
+        for start, end in sel.visible_spans(g, i):
+            mask[i, start:end] = True
+    return mask

@@ -1,0 +1,82 @@
+"""C-ABI library: loads without a GPU, exports every symbol declared in
+include/*.h, and its host-side logic (config validation, pooled counts,
+workspace sizing) agrees with the reference semantics."""
+
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+from paper_2509_24663_b200 import _lib
+from paper_2509_24663_b200.core import AttentionConfig, ConfigError, validate_config
+
+
+def _declared():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"\b(swattn_[a-z0-9_]+)\s*\(", src):
+            names.add(m.group(1))
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    declared = _declared()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(_lib.EXPORTED) == set(declared)
+
+
+BAD = [
+    dict(h_q=0), dict(k_top=-1), dict(h_q=31), dict(s_C1=40), dict(s_C2=200),
+    dict(l_C1=24, s_C1=16), dict(l=6), dict(N_local=3), dict(w=4096),
+]
+
+
+@pytest.mark.parametrize("kw", BAD)
+def test_validate_config_messages_match(kw):
+    cfg = AttentionConfig(**kw)
+    with pytest.raises(ConfigError) as py:
+        validate_config(cfg)
+    rc = _lib.lib().swattn_validate_config(_lib.c_config(cfg))
+    assert rc == _lib.SWATTN_EINVAL
+    assert _lib.last_error() == str(py.value)
+
+
+def test_reference_messages_verbatim():
+    # messages as produced by the reference (core.py:118-175)
+    with pytest.raises(ConfigError, match=r"^head-divisibility: h_q=30 is not a multiple of h_kv=4$"):
+        validate_config(AttentionConfig(h_q=30, h_kv=4))
+    with pytest.raises(ConfigError, match=r"^window-coverage: N_local=3 < ceil\(w/B\)\+1=32"):
+        validate_config(AttentionConfig(N_local=3))
+
+
+def test_default_config_is_supported_profile():
+    L = _lib.lib()
+    c = _lib.c_config(AttentionConfig())
+    assert L.swattn_validate_config(c) == 0
+    assert L.swattn_profile_supported(c) == 1
+    small = AttentionConfig(h_q=4, h_kv=2, d_h=16, B=16, l_C1=8, s_C1=4, l_C2=32, s_C2=16,
+                            N_local=2, k_top=3, w=16)
+    assert L.swattn_profile_supported(_lib.c_config(small)) == 0
+
+
+@pytest.mark.parametrize("n,l,s,m", [(80, 32, 16, 4), (31, 32, 16, 0), (32, 32, 16, 1),
+                                     (131072, 32, 16, 8191), (131072, 128, 64, 2047)])
+def test_num_pooled(n, l, s, m):
+    assert _lib.lib().swattn_num_pooled(n, l, s) == m
+
+
+def test_workspace_grows_with_n():
+    L = _lib.lib()
+    c = _lib.c_config(AttentionConfig())
+    a, b = L.swattn_workspace_bytes(c, 4096), L.swattn_workspace_bytes(c, 131072)
+    assert 0 < a < b
+    # S^cmp candidate region dominates at 128K: h_kv * n * 2048 * 4 bytes
+    assert b >= 2 * 131072 * 2048 * 4

@@ -1,0 +1,260 @@
+"""GPU parity: every hot-path kernel vs the reference-pinned golden vectors and
+the CPU oracle, through the C ABI (via the drop-in Python API).
+
+Bars (north star / SURVEY §8c):
+  * pooled keys, block indices: bit-exact (ties broken as the reference);
+  * S^cmp: relative error <= kScoreRelErr (4e-6) vs float64;
+  * attention O: max-abs <= 2e-2 and mean-abs <= 2e-3 vs the float64
+    reference values, lse abs <= 1e-3 (bf16 storage, fp32 softmax).
+"""
+
+import ml_dtypes
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from oracle import swattn_oracle as O
+from paper_2509_24663_b200 import _lib
+from paper_2509_24663_b200.compression import mean_pool_keys
+from paper_2509_24663_b200.core import AttentionConfig
+from paper_2509_24663_b200.dense import tiled_gqa_forward
+from paper_2509_24663_b200.selection import select_blocks
+from paper_2509_24663_b200.sparse import sparse_forward
+from paper_2509_24663_b200.switch import SwitchPolicy, attend
+
+pytestmark = pytest.mark.gpu
+
+O_MAX_ABS, O_MEAN_ABS, LSE_ABS = 2e-2, 2e-3, 1e-3
+SCORE_REL = 4e-6
+
+PAPER_GOLDEN = ["paper_n300_s5", "paper_n4096_s0", "paper_n8192_s0", "paper_n10000_s1",
+                "paper_n16384_s2"]
+SMALL_GOLDEN = ["small_n64_s0", "small_n257_s0", "small_n1000_s3"]
+
+
+def _cfgs(rec):
+    c = [int(x) for x in rec["cfg"]]
+    prof = O.Profile(h_q=c[0], h_kv=c[1], d_h=c[2], B=c[3], l_C1=c[4], s_C1=c[5], l_C2=c[6],
+                     s_C2=c[7], l=c[8], s=c[9], N_init=c[10], N_local=c[11], k_top=c[12],
+                     w=c[13])
+    cfg = AttentionConfig(h_q=c[0], h_kv=c[1], d_h=c[2], B=c[3], l_C1=c[4], s_C1=c[5],
+                          l_C2=c[6], s_C2=c[7], l=c[8], s=c[9], N_init=c[10], N_local=c[11],
+                          k_top=c[12], w=c[13])
+    return prof, cfg
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def _load(name):
+    rec = load_golden(name)
+    prof, cfg = _cfgs(rec)
+    Q, K, V = O.draw_qkv(int(rec["n"]), prof.h_q, prof.h_kv, prof.d_h, int(rec["seed"]))
+    assert O.digest(Q, K, V) == str(rec["digest"])
+    return rec, prof, cfg, (Q, K, V), (_dev(Q), _dev(K), _dev(V))
+
+
+def _host_bits(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("name", PAPER_GOLDEN + SMALL_GOLDEN)
+def test_k1_pooled_keys_bit_exact(name):
+    rec, prof, cfg, host, (Qd, Kd, Vd) = _load(name)
+    c1 = mean_pool_keys(Kd, cfg.l_C1, cfg.s_C1)
+    c2 = mean_pool_keys(Kd, cfg.l_C2, cfg.s_C2)
+    torch.cuda.synchronize()
+    assert O.digest(_host_bits(c1.keys)) == str(rec["c1_digest"])
+    assert O.digest(_host_bits(c2.keys)) == str(rec["c2_digest"])
+    # fused one-pass kernel (both profiles at once) through the raw C ABI
+    L = _lib.lib()
+    n = Kd.shape[0]
+    m1, m2 = L.swattn_num_pooled(n, cfg.l_C1, cfg.s_C1), L.swattn_num_pooled(n, cfg.l_C2, cfg.s_C2)
+    k1 = torch.empty((m1, cfg.h_kv, cfg.d_h), dtype=torch.bfloat16, device="cuda")
+    k2 = torch.empty((max(m2, 1), cfg.h_kv, cfg.d_h), dtype=torch.bfloat16, device="cuda")
+    _lib.check(L.swattn_compress_keys(_lib.c_config(cfg), Kd.data_ptr(), n, k1.data_ptr(),
+                                      k2.data_ptr() if m2 else None, _lib.stream_handle()), "k1")
+    torch.cuda.synchronize()
+    assert O.digest(_host_bits(k1)) == str(rec["c1_digest"])
+    if m2:
+        assert O.digest(_host_bits(k2[:m2])) == str(rec["c2_digest"])
+
+
+@pytest.mark.parametrize("name", PAPER_GOLDEN + SMALL_GOLDEN)
+def test_selection_bit_exact(name):
+    rec, prof, cfg, host, (Qd, Kd, Vd) = _load(name)
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    torch.cuda.synchronize()
+    k = cfg.k_top
+    got = sel.topk.cpu().numpy().astype(np.int64)
+    want = rec["topk"].astype(np.int64)[:, :, :k]
+    bad = np.argwhere((got != want).any(axis=2))
+    assert bad.size == 0, f"{len(bad)} rows differ, first {bad[:5].tolist()}; reranked={int(sel.n_reranked)}"
+    assert np.array_equal(sel.counts, rec["counts"].astype(np.int64))
+    if "topk_exact" in rec:
+        for mode in ("fused-exact", "exact"):
+            sel_e = select_blocks(Qd, Kd, cfg, mode=mode)
+            got_e = sel_e.topk.cpu().numpy().astype(np.int64)
+            assert np.array_equal(got_e, rec["topk_exact"].astype(np.int64)[:, :, :k]), mode
+
+
+@pytest.mark.parametrize("name", ["paper_n8192_s0", "paper_n16384_s2", "paper_n10000_s1"])
+def test_k2_score_error_bound(name):
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load(name)
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    n = Qd.shape[0]
+    c1 = mean_pool_keys(Kd, cfg.l_C1, cfg.s_C1).keys
+    c2 = mean_pool_keys(Kd, cfg.l_C2, cfg.s_C2).keys
+    m1 = c1.shape[0]
+    n_cols = -(-m1 // cfg.s)
+    ld = (n_cols + 3) // 4 * 4
+    scmp = torch.full((cfg.h_kv, n, ld), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.check(L.swattn_block_scores(c, Qd.data_ptr(), c1.data_ptr(), c2.data_ptr(), n, 2,
+                                     scmp.data_ptr(), ld, None, _lib.stream_handle()), "k2")
+    torch.cuda.synchronize()
+    rows = rec["score_rows"]
+    want = rec["cmp_approx"]  # [R, h_kv, n_cols] float64 from the reference
+    got = scmp.cpu().numpy()[:, rows, :n_cols].transpose(1, 0, 2)
+    worst = 0.0
+    for ri, i in enumerate(rows):
+        b = int(i) // cfg.B
+        hi = min(max(0, b - cfg.N_local + 1), n_cols)
+        if hi <= cfg.N_init:
+            continue
+        w = want[ri, :, cfg.N_init:hi]
+        g = got[ri, :, cfg.N_init:hi]
+        worst = max(worst, float(np.max(np.abs(g - w) / np.abs(w))))
+    print(f"{name}: max rel err of S^cmp = {worst:.3e}")
+    assert worst <= SCORE_REL
+
+
+def _tol(got_bf16_dev, want_f64, lse_dev, want_lse):
+    got = got_bf16_dev.float().cpu().numpy().astype(np.float64)
+    err = np.abs(got - want_f64)
+    assert err.max() <= O_MAX_ABS, err.max()
+    assert err.mean() <= O_MEAN_ABS, err.mean()
+    lerr = np.abs(lse_dev.cpu().numpy().astype(np.float64) - want_lse)
+    assert lerr.max() <= LSE_ABS, lerr.max()
+    return float(err.max()), float(err.mean()), float(lerr.max())
+
+
+@pytest.mark.parametrize("name", PAPER_GOLDEN)
+def test_sparse_attention_tolerance(name):
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load(name)
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    res = sparse_forward(Qd, Kd, Vd, sel, cfg)
+    torch.cuda.synchronize()
+    rows = rec["sparse_rows"]
+    top = rec["topk"].astype(np.int64)
+    if str(rec["sparse_mode"]) == "sparse":
+        want_o, want_l = O.sparse_attention(Q, K, V, top, prof, rows=rows)
+    else:
+        want_o, want_l = O.dense_attention(Q, K, V, prof, rows=rows)
+    r = torch.as_tensor(rows, device="cuda")
+    stats = _tol(res.output[r], want_o, res.lse[r], want_l)
+    # and against the reference's own bf16 output
+    ref_bf16 = rec["sparse_out_bits"].view(ml_dtypes.bfloat16).astype(np.float64)
+    got = res.output[r].float().cpu().numpy()
+    assert np.abs(got - ref_bf16).max() <= O_MAX_ABS
+    print(name, "sparse max/mean/lse err", stats)
+
+
+@pytest.mark.parametrize("name", ["paper_n300_s5", "paper_n4096_s0", "paper_n8192_s0"])
+def test_dense_attention_tolerance(name):
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load(name)
+    res = tiled_gqa_forward(Qd, Kd, Vd, cfg)
+    torch.cuda.synchronize()
+    rows = rec["dense_rows"]
+    want_o, want_l = O.dense_attention(Q, K, V, prof, rows=rows)
+    r = torch.as_tensor(rows, device="cuda")
+    print(name, "dense max/mean/lse err", _tol(res.output[r], want_o, res.lse[r], want_l))
+
+
+def test_attend_switch_dispatch():
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load("paper_n4096_s0")
+    res, mode = attend(Qd, Kd, Vd, cfg)
+    assert mode == "dense"  # 4096 <= 6144 (switch.py:69)
+    res_s, mode_s = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    assert mode_s == "sparse"
+    res_t, mode_t = attend(Qd, Kd, Vd, cfg, SwitchPolicy(threshold_tokens=4095))
+    assert mode_t == "sparse"
+    torch.cuda.synchronize()
+    # at 4K every causal block is selected (budget 96 >= 64 blocks): sparse == dense
+    d = (res.output.float() - res_s.output.float()).abs().max().item()
+    assert d <= 2e-2
+    assert torch.equal(res_s.output, res_t.output)
+    with pytest.raises(ValueError):
+        attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="bogus"))
+
+
+def test_attend_host_arrays_roundtrip():
+    rec, prof, cfg, (Q, K, V), _ = _load("paper_n8192_s0")
+    res, mode = attend(Q, K, V, cfg)  # numpy bf16 in -> numpy out (H2D/D2H inside)
+    assert mode == "sparse"
+    assert isinstance(res.output, np.ndarray) and res.output.dtype == ml_dtypes.bfloat16
+    rows = rec["sparse_rows"]
+    ref = rec["sparse_out_bits"].view(ml_dtypes.bfloat16).astype(np.float64)
+    assert np.abs(res.output[rows].astype(np.float64) - ref).max() <= O_MAX_ABS
+    assert np.abs(res.lse[rows] - rec["sparse_lse"]).max() <= LSE_ABS
+
+
+def test_determinism_bitwise():
+    rec, prof, cfg, _, (Qd, Kd, Vd) = _load("paper_n10000_s1")
+    outs = [attend(Qd, Kd, Vd, cfg)[0] for _ in range(2)]
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].output, outs[1].output)
+    assert torch.equal(outs[0].lse, outs[1].lse)
+
+
+def test_errors_match_reference_behaviour():
+    cfg = AttentionConfig()
+    Qd = torch.zeros((64, 32, 128), dtype=torch.bfloat16, device="cuda")
+    Kd = torch.zeros((64, 2, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="K shape"):
+        tiled_gqa_forward(Qd, Kd[:32], Kd[:32], cfg)
+    with pytest.raises(ValueError, match="unknown selection mode"):
+        select_blocks(Qd, Kd, cfg, mode="fast")
+    with pytest.raises(ValueError, match="tile sizes"):
+        select_blocks(Qd, Kd, cfg, B_q=0)
+
+
+def _random_rows(n, k, seed):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([rng.choice(n, size=k, replace=False), [n - 1, n // 2]]))
+
+
+@pytest.mark.parametrize("n,seed", [(32768, 11), (131072, 12)])
+def test_full_size_properties_and_sampled_rows(n, seed):
+    """BASELINE sizes: the oracle checks sampled rows exactly (selection) and
+    within tolerance (attention); size-independent properties cover the rest."""
+    prof, cfg = O.PAPER, AttentionConfig()
+    Q, K, V = O.draw_qkv(n, 32, 2, 128, seed)
+    Qd, Kd, Vd = _dev(Q), _dev(K), _dev(V)
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    res = sparse_forward(Qd, Kd, Vd, sel, cfg)
+    torch.cuda.synchronize()
+    top = sel.topk.cpu().numpy()
+    cnt = sel.topk_cnt.cpu().numpy()
+    i = np.arange(n)
+    b = i // 64
+    lo = np.maximum(0, b - 31)
+    ncand = np.maximum(0, np.minimum(lo, -(-O.n_pooled(n, 32, 16) // 4)) - 1)
+    assert np.array_equal(cnt, np.broadcast_to(np.minimum(63, ncand), cnt.shape))
+    valid = top >= 0
+    assert np.array_equal(valid.sum(axis=2), cnt)
+    # ascending, inside the candidate pool
+    t = np.where(valid, top, np.iinfo(np.int32).max)
+    assert np.all(np.diff(t, axis=2)[valid[:, :, 1:]] > 0)
+    assert np.all((top >= 1)[valid]) and np.all((top < lo[None, :, None])[valid])
+    rows = _random_rows(n, 24, seed)
+    want_top, _, _ = O.select(Q, K, prof, "approx", rows=rows)
+    assert np.array_equal(top[:, rows, :], want_top)
+    full = np.full((2, n, 63), -1, dtype=np.int64)
+    full[:, rows] = want_top
+    want_o, want_l = O.sparse_attention(Q, K, V, full, prof, rows=rows)
+    r = torch.as_tensor(rows, device="cuda")
+    print(n, "sampled-row sparse err", _tol(res.output[r], want_o, res.lse[r], want_l),
+          "reranked rows", int(sel.n_reranked))
