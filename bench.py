@@ -345,7 +345,8 @@ def stage_breakdown(L, c, cfg, Q, K, V, n, stream, reps=2):
         "K4_sparse_attention": lambda: L.swattn_sparse_fwd(c, Q.data_ptr(), K.data_ptr(),
                                                            V.data_ptr(), n, topk.data_ptr(),
                                                            cnt.data_ptr(), O_.data_ptr(),
-                                                           lse.data_ptr(), sh),
+                                                           lse.data_ptr(), work.data_ptr(), wsb,
+                                                           sh),
     }
     out = {}
     for name, fn in calls.items():

@@ -119,10 +119,14 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
 
 /* K4 -- sparse_forward (sparse.py:43-98): O [n, h_q, d_h] bf16, lse [n, h_q]
  * fp32 (natural log).  Visible set of row i per group = init U local U
- * topk[g, i] clipped causally (selection.py:73-87). */
+ * topk[g, i] clipped causally (selection.py:73-87).  Part A (init + local,
+ * shared per query block) and part B (per-token top-k) run as two tcgen05
+ * kernels; the workspace holds part A's row statistics. */
 int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K,
                           const void *V, int64_t n, const int32_t *topk,
-                          const int32_t *topk_cnt, void *O, float *lse, void *stream);
+                          const int32_t *topk_cnt, void *O, float *lse, void *workspace,
+                          size_t workspace_bytes, void *stream);
+size_t swattn_sparse_workspace_bytes(const swattn_config *cfg, int64_t n);
 
 /* K5 -- tiled_gqa_forward (dense.py:112-170): causal (or full) GQA flash
  * attention, O bf16, lse fp32. */

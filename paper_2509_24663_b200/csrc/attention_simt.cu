@@ -72,12 +72,11 @@ __device__ __forceinline__ void fold_range(const AttnArgs &a, const float *q_s, 
   }
 }
 
-__global__ void __launch_bounds__(kG * 32) attention_rows_kernel(AttnArgs a) {
+__device__ void attend_row(const AttnArgs &a, int64_t i, int g) {
   __shared__ float q_all[kG][kD];
   __shared__ int blocks_s[kMaxBlocks];
   __shared__ int nblocks_s;
-  const int64_t i = blockIdx.x;
-  const int g = blockIdx.y;
+  __syncthreads();  // smem reuse across rows of a persistent loop
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hq = g * a.G + warp;
   for (int t = threadIdx.x; t < kG * kD; t += blockDim.x)
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(kG * 32) attention_rows_kernel(AttnArgs a) {
   }
   if (l == 0.f) {
     if (lane == 0 && a.err != nullptr) atomicExch(a.err, 1);
-    return;
+    l = 1.f;  // empty visible set: flagged; keep the warp in lock-step
   }
   const float inv = 1.f / l;
   __nv_bfloat16 *o = a.O + (i * a.h_q + hq) * kD + lane * 4;
@@ -120,7 +119,50 @@ __global__ void __launch_bounds__(kG * 32) attention_rows_kernel(AttnArgs a) {
   if (lane == 0) a.lse[i * a.h_q + hq] = (m + __log2f(l)) * 0.6931471805599453f;
 }
 
+__global__ void __launch_bounds__(kG * 32) attention_rows_kernel(AttnArgs a) {
+  attend_row(a, blockIdx.x, blockIdx.y);
+}
+
+// exact recomputation of listed (group, token) rows (g * n + i)
+__global__ void __launch_bounds__(kG * 32) attention_list_kernel(AttnArgs a, const int32_t *count,
+                                                                 const int32_t *list) {
+  const int total = *count;
+  for (int e = blockIdx.x; e < total; e += gridDim.x) {
+    const int32_t row = list[e];
+    attend_row(a, row % a.n, (int)(row / a.n));
+  }
+}
+
 }  // namespace
+
+int32_t launch_attention_list(const swattn_config *cfg, const void *Q, const void *K,
+                              const void *V, int64_t n, const int32_t *topk,
+                              const int32_t *topk_cnt, const int32_t *count, const int32_t *list,
+                              void *O, float *lse, int grid, cudaStream_t stream) {
+  AttnArgs a;
+  a.Q = static_cast<const __nv_bfloat16 *>(Q);
+  a.K = static_cast<const __nv_bfloat16 *>(K);
+  a.V = static_cast<const __nv_bfloat16 *>(V);
+  a.n = n;
+  a.h_q = cfg->h_q;
+  a.h_kv = cfg->h_kv;
+  a.G = cfg->h_q / cfg->h_kv;
+  a.B = cfg->B;
+  a.N_init = cfg->N_init;
+  a.N_local = cfg->N_local;
+  a.k_top = cfg->k_top;
+  a.topk = topk;
+  a.topk_cnt = topk_cnt;
+  a.sparse = 1;
+  a.causal = 1;
+  a.scale_log2 = (1.f / sqrtf((float)cfg->d_h)) * 1.4426950408889634f;
+  a.O = static_cast<__nv_bfloat16 *>(O);
+  a.lse = lse;
+  a.err = nullptr;
+  attention_list_kernel<<<grid, kG * 32, 0, stream>>>(a, count, list);
+  SWATTN_LAUNCH_CHECK("attention_list_kernel");
+  return SWATTN_OK;
+}
 
 int32_t launch_attention_simt(const swattn_config *cfg, const void *Q, const void *K,
                               const void *V, int64_t n, const int32_t *topk,

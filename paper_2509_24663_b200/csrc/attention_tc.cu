@@ -1,0 +1,371 @@
+// K5 / K4-part-A -- block-list flash attention on tcgen05 (sm_100a).
+//
+// One CTA = one GQA-packed query tile of 128 rows = 8 tokens x 16 heads of
+// one KV group (row r <-> token t0 + r/16, head 16g + r%16), so every row of
+// the tile reads the same K/V blocks.  The tile walks a list of 64-key
+// blocks:
+//   dense (tiled_gqa_forward, dense.py:112-170): blocks 0..b, causal;
+//   sparse part A (sparse.py:43-98, the init + local blocks every token of a
+//   query block shares, selection.py:113-119): [0, n_init) U [lo, b].
+//
+// Warp roles (192 threads, 2 CTAs / SM):
+//   warp 0      TMA producer: Q once, then K and V blocks through two
+//               independent 2-stage rings (K freed after QK^T, V after PV);
+//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into a
+//               double-buffered TMEM S tile (128 x 64 fp32), then
+//               O += P_{j-1} V_{j-1} with P read straight from TMEM (kind::f16
+//               A-from-TMEM), O accumulated in TMEM (128 x 128 fp32);
+//   warps 2..5  softmax: thread = row; online max with lazy rescaling (O is
+//               rescaled in TMEM only when the row max grows by > 2^8),
+//               P = exp2(s*scale*log2e - m) packed to bf16 into the S buffer;
+//               epilogue O / l -> bf16, lse.
+// Roofline: tensor-bound; algorithmic FLOP = 4 * visible_pairs * d_h * h_q
+// (dense.py:167-169 counts x 2).
+#include <string.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+#include "tma_host.cuh"
+
+namespace swattn {
+
+namespace {
+
+constexpr int kRows = 128;         // query rows per tile
+constexpr int kTokTile = kRows / kG;  // 8 tokens
+constexpr int kBlk = 64;           // keys per block
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+constexpr uint32_t kQBytes = kRows * kD * 2;     // 32 KB
+constexpr uint32_t kKVBytes = kBlk * kD * 2;     // 16 KB
+constexpr uint32_t kTmemCols = 256;              // S0 | S1 | O
+constexpr float kRescaleThresh = 8.0f;           // log2 units
+
+struct FaParams {
+  CUtensorMap q_map;   // Q [n][h_q][d]: box {64, 16, 8}
+  CUtensorMap k_map;   // K [n][h_kv*d]: box {64, 64}
+  CUtensorMap v_map;
+  int64_t n;
+  int h_q, h_kv;
+  int n_tiles;         // token tiles of 8
+  int mode;            // 0 dense causal, 1 dense non-causal, 2 sparse part A
+  int N_init, N_local;
+  float scale_log2;
+  __nv_bfloat16 *O;
+  float *lse;          // [n][h_q]
+  float *m_out, *l_out;  // part A: per-row running max (log2) and sum, [n][h_q]
+};
+
+struct __align__(1024) FaSmem {
+  uint8_t q[kQBytes];
+  uint8_t k[kStages][kKVBytes];
+  uint8_t v[kStages][kKVBytes];
+  uint64_t q_full;
+  uint64_t k_full[kStages], k_empty[kStages];
+  uint64_t v_full[kStages], v_empty[kStages];
+  uint64_t s_full[2], p_full[2];
+  uint64_t o_done, o_final;
+  uint32_t tmem_base;
+};
+
+// Block list of a tile (query block b): dense 0..b / 0..nb-1, part A init U local.
+struct BlockList {
+  int n_first, first_end;  // [0, first_end)
+  int second_begin, second_end;  // [second_begin, second_end)
+  __device__ int size() const { return first_end + (second_end - second_begin); }
+  __device__ int at(int i) const { return i < first_end ? i : second_begin + (i - first_end); }
+};
+
+__device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t nb_total) {
+  BlockList L;
+  if (p.mode == 2) {
+    const int n_init = min(p.N_init, b + 1);
+    const int lo = max(0, b - p.N_local + 1);
+    L.first_end = n_init;
+    L.second_begin = max(lo, n_init);
+    L.second_end = b + 1;
+  } else {
+    L.first_end = (p.mode == 0) ? b + 1 : (int)nb_total;
+    L.second_begin = 0;
+    L.second_end = 0;
+  }
+  L.n_first = 0;
+  return L;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_constant__ FaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  FaSmem &s = *reinterpret_cast<FaSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                          ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // heavy (late) tiles first: causal work grows with the token index
+  const int tile = p.n_tiles - 1 - (int)blockIdx.x;
+  const int g = blockIdx.y;
+  const int64_t t0 = (int64_t)tile * kTokTile;
+  const int b = (int)(t0 / kBlk);
+  const int64_t nb_total = cdiv(p.n, kBlk);
+  const BlockList L = make_list(p, b, nb_total);
+  const int nblk = L.size();
+
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&s.q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.k_full[i], 1);
+      tc::mbar_init(&s.k_empty[i], 1);
+      tc::mbar_init(&s.v_full[i], 1);
+      tc::mbar_init(&s.v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s.s_full[i], 1);
+      tc::mbar_init(&s.p_full[i], 128);
+    }
+    tc::mbar_init(&s.o_done, 1);
+    tc::mbar_init(&s.o_final, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<kTmemCols>(&s.tmem_base);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  const uint32_t tmem_o = tmem + 128;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (tc::elect_one()) {
+      tc::tma_prefetch(&p.q_map);
+      tc::tma_prefetch(&p.k_map);
+      tc::tma_prefetch(&p.v_map);
+      tc::mbar_arrive_expect_tx(&s.q_full, kQBytes);
+      for (int h = 0; h < 2; ++h)
+        tc::tma_load_3d(&p.q_map, &s.q_full, s.q + h * (kQBytes / 2), h * 64, g * kG, (int)t0);
+      for (int i = 0; i < nblk; ++i) {
+        const int st = i % kStages;
+        const uint32_t ph = ((i / kStages) & 1) ^ 1;
+        const int key0 = L.at(i) * kBlk;
+        tc::mbar_wait(&s.k_empty[st], ph);
+        tc::mbar_arrive_expect_tx(&s.k_full[st], kKVBytes);
+        for (int h = 0; h < 2; ++h)
+          tc::tma_load_2d(&p.k_map, &s.k_full[st], s.k[st] + h * (kKVBytes / 2), g * kD + h * 64,
+                          key0);
+        tc::mbar_wait(&s.v_empty[st], ph);
+        tc::mbar_arrive_expect_tx(&s.v_full[st], kKVBytes);
+        for (int h = 0; h < 2; ++h)
+          tc::tma_load_2d(&p.v_map, &s.v_full[st], s.v[st] + h * (kKVBytes / 2), g * kD + h * 64,
+                          key0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t id_s = tc::idesc_bf16(kRows, kBlk, false, false);
+    const uint32_t id_o = tc::idesc_bf16(kRows, kD, false, true);
+    const uint32_t q_addr = tc::smem_u32(s.q);
+    tc::mbar_wait(&s.q_full, 0);
+    tc::tc_fence_after();
+    for (int i = 0; i <= nblk; ++i) {
+      if (i < nblk) {
+        const int st = i % kStages;
+        tc::mbar_wait(&s.k_full[st], (i / kStages) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint32_t k_addr = tc::smem_u32(s.k[st]);
+          const uint32_t d_s = tmem + (i & 1) * kBlk;
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const int h = kk >> 2, j = kk & 3;
+            tc::mma_ss(d_s, tc::desc_kmajor(q_addr + h * (kQBytes / 2) + j * 32),
+                       tc::desc_kmajor(k_addr + h * (kKVBytes / 2) + j * 32), id_s, kk > 0);
+          }
+          tc::mma_commit(&s.s_full[i & 1]);
+          tc::mma_commit(&s.k_empty[st]);
+        }
+        __syncwarp();
+      }
+      if (i >= 1) {
+        const int pi = i - 1;
+        const int st = pi % kStages;
+        tc::mbar_wait(&s.p_full[pi & 1], (pi >> 1) & 1);
+        tc::mbar_wait(&s.v_full[st], (pi / kStages) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint32_t v_addr = tc::smem_u32(s.v[st]);
+          const uint32_t a_p = tmem + (pi & 1) * kBlk;
+#pragma unroll
+          for (int kk = 0; kk < kBlk / 16; ++kk)
+            tc::mma_ts(tmem_o, a_p + kk * 8, tc::desc_mnmajor(v_addr + kk * 16 * 128, kKVBytes / 2),
+                       id_o, (pi > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_commit(&s.v_empty[st]);
+          tc::mma_commit(&s.o_done);
+          if (pi == nblk - 1) tc::mma_commit(&s.o_final);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int64_t tok = t0 + r / kG;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int i = 0; i < nblk; ++i) {
+      const int jb = L.at(i);
+      tc::mbar_wait(&s.s_full[i & 1], (i >> 1) & 1);
+      tc::tc_fence_after();
+      uint32_t ra[32], rb[32];
+      tc::tmem_ld32(tmem + lane_off + (i & 1) * kBlk, ra);
+      tc::tmem_ld32(tmem + lane_off + (i & 1) * kBlk + 32, rb);
+      tc::tmem_ld_wait();
+      float x[kBlk];
+      const int64_t key0 = (int64_t)jb * kBlk;
+      const bool diag = (p.mode != 1) && (key0 + kBlk - 1 > tok);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kBlk; ++c) {
+        float v = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]) * p.scale_log2;
+        if (diag && key0 + c > tok) v = -INFINITY;
+        if (p.mode == 1 && key0 + c >= p.n) v = -INFINITY;
+        x[c] = v;
+        mx = fmaxf(mx, v);
+      }
+      if (mx > m + kRescaleThresh || m == -INFINITY) {
+        const float m_new = fmaxf(mx, m);
+        if (m != -INFINITY && i > 0) {
+          // S_i completing implies PV_{i-2} completed (issue order S_i after
+          // PV_{i-2}), so o_done has 0 or 1 pending phase: the parity wait
+          // for completion #i (PV_{i-1}) is unambiguous.
+          const float alpha = fast_exp2(m - m_new);
+          tc::mbar_wait(&s.o_done, (i - 1) & 1);
+          tc::tc_fence_after();
+#pragma unroll
+          for (int c0 = 0; c0 < kD; c0 += 32) {
+            uint32_t o[32];
+            tc::tmem_ld32(tmem_o + lane_off + c0, o);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tc::tmem_st32(tmem_o + lane_off + c0, o);
+          }
+          l *= alpha;
+        }
+        m = m_new;
+      }
+      uint32_t pk[kBlk / 2];
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < kBlk; c += 2) {
+        const float p0 = fast_exp2(x[c] - m);
+        const float p1 = fast_exp2(x[c + 1] - m);
+        rs += p0 + p1;
+        pk[c / 2] = tc::pack_bf16(p0, p1);
+      }
+      l += rs;
+      tc::tmem_st32(tmem + lane_off + (i & 1) * kBlk, pk);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&s.p_full[i & 1]);
+    }
+    // epilogue: PV_{nblk-2} and PV_{nblk-1} may both be in flight here, which a
+    // parity wait on o_done cannot tell apart -> dedicated single-phase barrier
+    tc::mbar_wait(&s.o_final, 0);
+    tc::tc_fence_after();
+    const bool valid = tok < p.n;
+    const int hq = g * kG + (r % kG);
+    const float inv_l = 1.f / l;
+    __nv_bfloat16 *orow = p.O + ((int64_t)tok * p.h_q + hq) * kD;
+#pragma unroll
+    for (int c0 = 0; c0 < kD; c0 += 32) {
+      uint32_t o[32];
+      tc::tmem_ld32(tmem_o + lane_off + c0, o);
+      tc::tmem_ld_wait();
+      if (valid) {
+        uint4 *dst = reinterpret_cast<uint4 *>(orow + c0);
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 w;
+          w.x = tc::pack_bf16(__uint_as_float(o[e]) * inv_l, __uint_as_float(o[e + 1]) * inv_l);
+          w.y = tc::pack_bf16(__uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l);
+          w.z = tc::pack_bf16(__uint_as_float(o[e + 4]) * inv_l, __uint_as_float(o[e + 5]) * inv_l);
+          w.w = tc::pack_bf16(__uint_as_float(o[e + 6]) * inv_l, __uint_as_float(o[e + 7]) * inv_l);
+          dst[e / 8] = w;
+        }
+      }
+    }
+    if (valid) {
+      const int64_t idx = tok * p.h_q + hq;
+      p.lse[idx] = (m + __log2f(l)) * 0.6931471805599453f;
+      if (p.m_out != nullptr) {
+        p.m_out[idx] = m;
+        p.l_out[idx] = l;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
+}  // namespace
+
+bool attention_tc_available() { return true; }
+
+static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                         int64_t n, int mode, void *O, float *lse, float *m_out, float *l_out,
+                         cudaStream_t stream) {
+  FaParams p;
+  memset(&p, 0, sizeof(p));
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cfg->h_q, (uint64_t)n};
+    const uint64_t str[2] = {(uint64_t)kD * 2, (uint64_t)cfg->h_q * kD * 2};
+    const uint32_t box[3] = {64, (uint32_t)kG, (uint32_t)kTokTile};
+    if (!make_tmap_bf16(&p.q_map, Q, 3, dims, str, box)) {
+      set_error("cuTensorMapEncodeTiled(Q) failed");
+      return SWATTN_ECUDA;
+    }
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)cfg->h_kv * kD, (uint64_t)n};
+    const uint64_t str[1] = {(uint64_t)cfg->h_kv * kD * 2};
+    const uint32_t box[2] = {64, (uint32_t)kBlk};
+    if (!make_tmap_bf16(&p.k_map, K, 2, dims, str, box) ||
+        !make_tmap_bf16(&p.v_map, V, 2, dims, str, box)) {
+      set_error("cuTensorMapEncodeTiled(K/V) failed");
+      return SWATTN_ECUDA;
+    }
+  }
+  p.n = n;
+  p.h_q = cfg->h_q;
+  p.h_kv = cfg->h_kv;
+  p.n_tiles = (int)cdiv(n, kTokTile);
+  p.mode = mode;
+  p.N_init = cfg->N_init;
+  p.N_local = cfg->N_local;
+  p.scale_log2 = (1.f / sqrtf((float)cfg->d_h)) * 1.4426950408889634f;
+  p.O = static_cast<__nv_bfloat16 *>(O);
+  p.lse = lse;
+  p.m_out = m_out;
+  p.l_out = l_out;
+  const size_t smem = sizeof(FaSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fa_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid((unsigned)p.n_tiles, (unsigned)cfg->h_kv);
+  fa_tile_kernel<<<grid, kThreads, smem, stream>>>(p);
+  SWATTN_LAUNCH_CHECK("fa_tile_kernel");
+  return SWATTN_OK;
+}
+
+int32_t launch_dense_tc(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                        int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
+  return launch_fa(cfg, Q, K, V, n, causal ? 0 : 1, O, lse, nullptr, nullptr, stream);
+}
+
+int32_t launch_sparse_part_a(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                             int64_t n, void *O, float *lse, float *m_out, float *l_out,
+                             cudaStream_t stream) {
+  return launch_fa(cfg, Q, K, V, n, 2, O, lse, m_out, l_out, stream);
+}
+
+}  // namespace swattn

@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -43,8 +44,15 @@ int32_t launch_rerank(const swattn_config *, const void *, const void *, const v
 int32_t launch_attention_simt(const swattn_config *, const void *, const void *, const void *,
                               int64_t, const int32_t *, const int32_t *, int, int, void *, float *,
                               int *, cudaStream_t);
-int32_t launch_sparse_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
-                         const int32_t *, const int32_t *, void *, float *, cudaStream_t);
+int32_t launch_sparse_part_a(const swattn_config *, const void *, const void *, const void *,
+                             int64_t, void *, float *, float *, float *, cudaStream_t);
+int32_t launch_sparse_part_b(const swattn_config *, const void *, const void *, const void *,
+                             int64_t, const int32_t *, const int32_t *, const float *,
+                             const float *, void *, float *, int32_t *, int32_t *, int,
+                             cudaStream_t);
+int32_t launch_attention_list(const swattn_config *, const void *, const void *, const void *,
+                              int64_t, const int32_t *, const int32_t *, const int32_t *,
+                              const int32_t *, void *, float *, int, cudaStream_t);
 int32_t launch_dense_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
                         int, void *, float *, cudaStream_t);
 bool scores_tc_available();
@@ -59,6 +67,18 @@ static int num_sms() {
     if (sms <= 0) sms = 148;
   }
   return sms;
+}
+
+// SWATTN_FORCE_SIMT=1 routes K2/K4/K5 to the CUDA-core kernels (A/B checks).
+static bool use_tc_scores() {
+  static int v = -1;
+  if (v < 0) v = getenv("SWATTN_FORCE_SIMT") == nullptr;
+  return v && scores_tc_available();
+}
+static bool use_tc_attention() {
+  static int v = -1;
+  if (v < 0) v = getenv("SWATTN_FORCE_SIMT") == nullptr;
+  return v && attention_tc_available();
 }
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -176,12 +196,19 @@ int64_t swattn_num_pooled(int64_t n, int32_t length, int32_t stride) {
   return num_pooled(n, length, stride);
 }
 
+size_t swattn_sparse_workspace_bytes(const swattn_config *cfg, int64_t n) {
+  if (cfg == nullptr || n < 1) return 0;
+  // part A row statistics m, l [n][h_q] fp32 + slow-path list
+  return 2 * align_up((size_t)n * cfg->h_q * 4) + align_up(16) +
+         align_up((size_t)cfg->h_kv * n * 4);
+}
+
 size_t swattn_workspace_bytes(const swattn_config *cfg, int64_t n) {
   if (cfg == nullptr || n < 1) return 0;
   const SelectLayout L = select_layout(cfg, n);
-  // attend additionally keeps the top-k lists
+  // attend additionally keeps the top-k lists and the sparse workspace
   return align_up(L.total) + align_up((size_t)cfg->h_kv * n * cfg->k_top * 4) +
-         align_up((size_t)cfg->h_kv * n * 4) + 256;
+         align_up((size_t)cfg->h_kv * n * 4) + swattn_sparse_workspace_bytes(cfg, n) + 256;
 }
 
 int32_t swattn_compress_keys(const swattn_config *cfg, const void *K, int64_t n, void *kc1,
@@ -218,7 +245,7 @@ int32_t swattn_block_scores(const swattn_config *cfg, const void *Q, const void 
     return SWATTN_EINVAL;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (scores_tc_available())
+  if (use_tc_scores())
     return launch_scores_tc(cfg, Q, kc1, kc2, n, mode, s_cmp, ld, flags, L.ld_f, st);
   return launch_scores_simt(cfg, Q, kc1, kc2, n, mode, s_cmp, ld, flags, L.ld_f, st);
 }
@@ -300,7 +327,7 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
     if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
     return rc;
   }
-  if (scores_tc_available())
+  if (use_tc_scores())
     rc = launch_scores_tc(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
   else
     rc = launch_scores_simt(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
@@ -320,7 +347,7 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
 
 int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                           int64_t n, const int32_t *topk, const int32_t *topk_cnt, void *O,
-                          float *lse, void *stream) {
+                          float *lse, void *workspace, size_t workspace_bytes, void *stream) {
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;
   if (n < 1) {
@@ -332,8 +359,26 @@ int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K
     return SWATTN_EUNSUPPORTED;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (attention_tc_available() && swattn_profile_supported(cfg))
-    return launch_sparse_tc(cfg, Q, K, V, n, topk, topk_cnt, O, lse, st);
+  if (use_tc_attention() && swattn_profile_supported(cfg)) {
+    const size_t need = swattn_sparse_workspace_bytes(cfg, n);
+    if (workspace == nullptr || workspace_bytes < need) {
+      set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
+      return SWATTN_EINVAL;
+    }
+    char *ws = static_cast<char *>(workspace);
+    float *m_a = reinterpret_cast<float *>(ws);
+    float *l_a = reinterpret_cast<float *>(ws + align_up((size_t)n * cfg->h_q * 4));
+    int32_t *slow_count = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4));
+    int32_t *slow_list = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4) +
+                                                     align_up(16));
+    if ((rc = launch_sparse_part_a(cfg, Q, K, V, n, O, lse, m_a, l_a, st))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(slow_count, 0, 4, st), "memset(slow)"))) return rc;
+    if ((rc = launch_sparse_part_b(cfg, Q, K, V, n, topk, topk_cnt, m_a, l_a, O, lse, slow_count,
+                                   slow_list, num_sms(), st)))
+      return rc;
+    return launch_attention_list(cfg, Q, K, V, n, topk, topk_cnt, slow_count, slow_list, O, lse,
+                                 num_sms(), st);
+  }
   return launch_attention_simt(cfg, Q, K, V, n, topk, topk_cnt, 1, 1, O, lse, nullptr, st);
 }
 
@@ -350,7 +395,7 @@ int32_t swattn_dense_fwd(const swattn_config *cfg, const void *Q, const void *K,
     return SWATTN_EUNSUPPORTED;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (attention_tc_available())
+  if (use_tc_attention())
     return launch_dense_tc(cfg, Q, K, V, n, causal, O, lse, st);
   return launch_attention_simt(cfg, Q, K, V, n, nullptr, nullptr, 0, causal, O, lse, nullptr, st);
 }
@@ -384,7 +429,10 @@ int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, co
   if ((rc = swattn_select_blocks(cfg, Q, K, n, select_mode, topk, cnt, nullptr, workspace, L.total,
                                  stream)))
     return rc;
-  return swattn_sparse_fwd(cfg, Q, K, V, n, topk, cnt, O, lse, stream);
+  char *sws = ws + align_up(L.total) + align_up((size_t)cfg->h_kv * n * cfg->k_top * 4) +
+              align_up((size_t)cfg->h_kv * n * 4);
+  return swattn_sparse_fwd(cfg, Q, K, V, n, topk, cnt, O, lse, sws,
+                           swattn_sparse_workspace_bytes(cfg, n), stream);
 }
 
 }  // extern "C"

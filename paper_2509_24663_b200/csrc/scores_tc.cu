@@ -1,0 +1,327 @@
+// K2 -- fused two-pass block scoring on tcgen05 (sm_100a).
+//
+// CTA = 8 query tokens x 16 heads of one KV group (128 rows), 2 CTAs / SM.
+//   Pass 1 (normal orientation, selection.py:165-196): S = Q_tile . K_C2^T
+//     over 128-column chunks of the normaliser keys (C2 for approx, C1 for
+//     exact); one thread per (token, head) row keeps the online (max, sum)
+//     in registers -> m, 1/l per row (log2 domain).
+//   Pass 2 (swap-AB, selection.py:199-222): S^T = K_C1_tile . Q_tile^T with
+//     M = 128 C1 columns, N = 128 (token, head) rows, so one thread owns one
+//     compressed column and the 16-head group sum
+//       shared(i, c) = sum_h exp2(s_h c' - m_h) / l_h
+//     is thread-local.  The 5/4 max-pool (compression.py:160-173) runs on
+//     warp shuffles; tiles advance by 124 columns so every 5-column window
+//     of the tile's 31 blocks is inside the tile.  Only the top-k candidate
+//     region [N_init, min(b - N_local + 1, n_cols)) is computed and written
+//     (S^cmp fp32), plus the argmax-at-shared-column flag bits K3 uses to
+//     classify exact ties.
+// Warp roles (192 threads): warp 0 TMA (Q once; C2 chunks then C1 tiles
+// through one 2-stage ring), warp 1 MMA issuer, warps 2..5 epilogues.
+// Roofline: tensor + MUFU; FLOP = 2 * h_q * d * (pass-1 cols + pass-2 cols)
+// per row (bench.py:144-155).
+#include <string.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+#include "tma_host.cuh"
+
+namespace swattn {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kTok = 8;
+constexpr int kRows = kTok * kG;           // 128
+constexpr int kCols = 128;                 // columns per chunk / tile
+constexpr int kTileBlocks = 31;
+constexpr int kTileStride = kTileBlocks * kPoolS;  // 124
+constexpr int kStages = 2;
+constexpr uint32_t kQBytes = kRows * kD * 2;      // 32 KB
+constexpr uint32_t kKBytes = kCols * kD * 2;      // 32 KB
+constexpr uint32_t kTmemCols = 256;
+
+struct ScParams {
+  CUtensorMap q_map;    // Q [n][h_q][d]: box {64, 16, 8}
+  CUtensorMap k1_map;   // K_C1 [m1][h_kv*d]: box {64, 128}
+  CUtensorMap k2_map;   // K_C2 (or K_C1 again in exact mode)
+  int64_t n, m1, m2;
+  int h_q, h_kv;
+  int l_C1, s_C1, l_C2, s_C2;
+  int N_init, N_local, B, n_cols;
+  int approx;
+  float scale_log2;
+  int64_t tok0;
+  int n_tiles_tok;      // CTAs along tokens
+  float *s_cmp;
+  int64_t ld;
+  uint64_t *flags;
+  int64_t ld_f;
+};
+
+struct __align__(1024) ScSmem {
+  uint8_t q[kQBytes];
+  uint8_t k[kStages][kKBytes];
+  uint64_t q_full, full[kStages], empty[kStages], tfull[2], tempty[2];
+  float2 stat[kRows];          // (m, 1/l) per (token, head) row, log2 domain
+  uint32_t edge[4][kTok];      // warp-boundary column values for the max-pool
+  unsigned long long fl[kTok];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_constant__ ScParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  ScSmem &s = *reinterpret_cast<ScSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                          ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // heavy CTAs (late tokens) first
+  const int tt = p.n_tiles_tok - 1 - (int)blockIdx.x;
+  const int g = blockIdx.y;
+  const int64_t i0 = p.tok0 + (int64_t)tt * kTok;
+  const int64_t i_last = min(i0 + kTok - 1, p.n - 1);
+  const int b = (int)(i0 / p.B);
+  const int hi = cand_hi(b, p.N_local, p.n_cols);
+  const int n_t2 = (hi + kTileBlocks - 1) / kTileBlocks;  // pass-2 tiles
+  const bool use_c2 = p.approx && vis_count(i0, p.l_C2, p.s_C2) > 0;
+  const int64_t vmax = use_c2 ? vis_count(i_last, p.l_C2, p.s_C2) : vis_count(i_last, p.l_C1, p.s_C1);
+  const int n_c1 = (int)cdiv(vmax, kCols);  // pass-1 chunks
+  const int n_units = n_c1 + n_t2;
+
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&s.q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.full[i], 1);
+      tc::mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s.tfull[i], 1);
+      tc::mbar_init(&s.tempty[i], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<kTmemCols>(&s.tmem_base);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      tc::tma_prefetch(&p.q_map);
+      tc::tma_prefetch(&p.k1_map);
+      tc::tma_prefetch(&p.k2_map);
+      tc::mbar_arrive_expect_tx(&s.q_full, kQBytes);
+      for (int h = 0; h < 2; ++h)
+        tc::tma_load_3d(&p.q_map, &s.q_full, s.q + h * (kQBytes / 2), h * 64, g * kG, (int)i0);
+      for (int u = 0; u < n_units; ++u) {
+        const int st = u % kStages;
+        tc::mbar_wait(&s.empty[st], ((u / kStages) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&s.full[st], kKBytes);
+        const bool p1 = u < n_c1;
+        const CUtensorMap *map = p1 ? (use_c2 ? &p.k2_map : &p.k1_map) : &p.k1_map;
+        const int row0 = p1 ? u * kCols : (u - n_c1) * kTileStride;
+        for (int h = 0; h < 2; ++h)
+          tc::tma_load_2d(map, &s.full[st], s.k[st] + h * (kKBytes / 2), g * kD + h * 64, row0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = tc::idesc_bf16(128, 128, false, false);
+    const uint32_t q_addr = tc::smem_u32(s.q);
+    tc::mbar_wait(&s.q_full, 0);
+    for (int u = 0; u < n_units; ++u) {
+      const int st = u % kStages, tb = u & 1;
+      tc::mbar_wait(&s.full[st], (u / kStages) & 1);
+      tc::mbar_wait(&s.tempty[tb], ((u >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t k_addr = tc::smem_u32(s.k[st]);
+        const bool p1 = u < n_c1;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const int h = kk >> 2, j = kk & 3;
+          const uint64_t dq = tc::desc_kmajor(q_addr + h * (kQBytes / 2) + j * 32);
+          const uint64_t dk = tc::desc_kmajor(k_addr + h * (kKBytes / 2) + j * 32);
+          // pass 1: rows = (token, head), cols = keys; pass 2: rows = C1 columns
+          tc::mma_ss(tmem + tb * kCols, p1 ? dq : dk, p1 ? dk : dq, idesc, kk > 0);
+        }
+        tc::mma_commit(&s.tfull[tb]);
+        tc::mma_commit(&s.empty[st]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    // ---------------- pass 1: thread = row (token r/16, head r%16)
+    const int64_t my_tok = min(i0 + r / kG, p.n - 1);
+    const int64_t my_vis = use_c2 ? vis_count(my_tok, p.l_C2, p.s_C2) : vis_count(my_tok, p.l_C1, p.s_C1);
+    float m = -INFINITY, l = 0.f;
+    for (int u = 0; u < n_c1; ++u) {
+      const int tb = u & 1;
+      tc::mbar_wait(&s.tfull[tb], (u >> 1) & 1);
+      tc::tc_fence_after();
+      const int64_t c0 = (int64_t)u * kCols;
+#pragma unroll
+      for (int q = 0; q < kCols; q += 32) {
+        uint32_t v[32];
+        tc::tmem_ld32(tmem + lane_off + tb * kCols + q, v);
+        tc::tmem_ld_wait();
+        float x[32];
+        float cm = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          x[e] = (c0 + q + e < my_vis) ? __uint_as_float(v[e]) * p.scale_log2 : -INFINITY;
+          cm = fmaxf(cm, x[e]);
+        }
+        if (cm > m) {
+          l *= fast_exp2(m - cm);
+          m = cm;
+        }
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc += fast_exp2(x[e] - m);
+        if (m != -INFINITY) l += acc;
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&s.tempty[tb]);
+    }
+    s.stat[r] = make_float2(m == -INFINITY ? 0.f : m, l > 0.f ? 1.f / l : 0.f);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+
+    // ---------------- pass 2: thread = C1 column of the tile
+    for (int t = 0; t < n_t2; ++t) {
+      const int u = n_c1 + t;
+      const int tb = u & 1;
+      const int64_t col = (int64_t)t * kTileStride + r;
+      tc::mbar_wait(&s.tfull[tb], (u >> 1) & 1);
+      tc::tc_fence_after();
+      float sc[kTok];
+#pragma unroll
+      for (int k = 0; k < kTok; ++k) {
+        uint32_t v[kG];
+        tc::tmem_ld16(tmem + lane_off + tb * kCols + k * kG, v);
+        tc::tmem_ld_wait();
+        float acc = 0.f;
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
+          const float2 st = s.stat[k * kG + h];
+          acc = fmaf(fast_exp2(fmaf(__uint_as_float(v[h]), p.scale_log2, -st.x)), st.y, acc);
+        }
+        const int64_t tok = i0 + k;
+        const int64_t v1 = vis_count(tok, p.l_C1, p.s_C1);
+        sc[k] = (col >= p.m1) ? -INFINITY : ((col < v1) ? acc : 0.f);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&s.tempty[tb]);
+      // warp-boundary column (lane 0 of the next warp) for blocks 7, 15, 23
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kTok; ++k) s.edge[quad][k] = __float_as_uint(sc[k]);
+      }
+      if (r < kTok) s.fl[r] = 0ull;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int qb = r >> 2;                  // block within the tile
+      const bool head_lane = (r & 3) == 0 && qb < kTileBlocks;
+      const int j = t * kTileBlocks + qb;     // global block index
+      const bool write = head_lane && j >= p.N_init && j < hi;
+#pragma unroll
+      for (int k = 0; k < kTok; ++k) {
+        const float v0 = sc[k];
+        const float v1 = __shfl_down_sync(0xffffffffu, v0, 1);
+        const float v2 = __shfl_down_sync(0xffffffffu, v0, 2);
+        const float v3 = __shfl_down_sync(0xffffffffu, v0, 3);
+        float v4 = __shfl_down_sync(0xffffffffu, v0, 4);
+        if (lane == 28) v4 = __uint_as_float(s.edge[(quad + 1) & 3][k]);
+        const float mx = fmaxf(fmaxf(fmaxf(v0, v1), fmaxf(v2, v3)), v4);
+        const int64_t tok = i0 + k;
+        if (write && tok < p.n) {
+          p.s_cmp[((int64_t)g * p.n + tok) * p.ld + j] = mx;
+          if (p.flags != nullptr) {
+            const float f = 1.f + 4.f * kScoreRelErr;
+            const bool L = v1 * f < v0 && v2 * f < v0 && v3 * f < v0 && v4 * f < v0;
+            const bool R = v0 * f < v4 && v1 * f < v4 && v2 * f < v4 && v3 * f < v4;
+            const unsigned long long bits =
+                ((unsigned long long)L << (2 * qb)) | ((unsigned long long)R << (2 * qb + 1));
+            if (bits) atomicOr(&s.fl[k], bits);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (p.flags != nullptr && r < kTok && i0 + r < p.n)
+        p.flags[((int64_t)g * p.n + i0 + r) * p.ld_f + t] = s.fl[r];
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
+}  // namespace
+
+bool scores_tc_available() { return true; }
+
+int32_t launch_scores_tc(const swattn_config *cfg, const void *Q, const void *kc1, const void *kc2,
+                         int64_t n, int32_t mode, float *s_cmp, int64_t ld, uint64_t *flags,
+                         int64_t ld_f, cudaStream_t stream) {
+  ScParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = n;
+  p.m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
+  p.m2 = num_pooled(n, cfg->l_C2, cfg->s_C2);
+  p.h_q = cfg->h_q;
+  p.h_kv = cfg->h_kv;
+  p.l_C1 = cfg->l_C1; p.s_C1 = cfg->s_C1; p.l_C2 = cfg->l_C2; p.s_C2 = cfg->s_C2;
+  p.N_init = cfg->N_init;
+  p.N_local = cfg->N_local;
+  p.B = cfg->B;
+  p.n_cols = (int)(p.m1 ? cdiv(p.m1, cfg->s) : 0);
+  p.approx = mode == SWATTN_SELECT_APPROX && p.m2 > 0;
+  const float scale = cfg->scale_compressed_logits ? 1.f / sqrtf((float)cfg->d_h) : 1.f;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.tok0 = (int64_t)(cfg->N_init + cfg->N_local) * cfg->B;
+  if (p.tok0 >= n || p.n_cols <= cfg->N_init) return SWATTN_OK;
+  p.n_tiles_tok = (int)cdiv(n - p.tok0, kTok);
+  p.s_cmp = s_cmp;
+  p.ld = ld;
+  p.flags = flags;
+  p.ld_f = ld_f;
+  {
+    const uint64_t dims[3] = {(uint64_t)kD, (uint64_t)cfg->h_q, (uint64_t)n};
+    const uint64_t str[2] = {(uint64_t)kD * 2, (uint64_t)cfg->h_q * kD * 2};
+    const uint32_t box[3] = {64, (uint32_t)kG, (uint32_t)kTok};
+    if (!make_tmap_bf16(&p.q_map, Q, 3, dims, str, box)) {
+      set_error("cuTensorMapEncodeTiled(Q) failed");
+      return SWATTN_ECUDA;
+    }
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)cfg->h_kv * kD, (uint64_t)p.m1};
+    const uint64_t str[1] = {(uint64_t)cfg->h_kv * kD * 2};
+    const uint32_t box[2] = {64, (uint32_t)kCols};
+    if (!make_tmap_bf16(&p.k1_map, kc1, 2, dims, str, box)) {
+      set_error("cuTensorMapEncodeTiled(K_C1) failed");
+      return SWATTN_ECUDA;
+    }
+    if (p.approx) {
+      const uint64_t dims2[2] = {(uint64_t)cfg->h_kv * kD, (uint64_t)p.m2};
+      if (!make_tmap_bf16(&p.k2_map, kc2, 2, dims2, str, box)) {
+        set_error("cuTensorMapEncodeTiled(K_C2) failed");
+        return SWATTN_ECUDA;
+      }
+    } else {
+      p.k2_map = p.k1_map;
+    }
+  }
+  const size_t smem = sizeof(ScSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid((unsigned)p.n_tiles_tok, (unsigned)cfg->h_kv);
+  scores_tc_kernel<<<grid, kThreads, smem, stream>>>(p);
+  SWATTN_LAUNCH_CHECK("scores_tc_kernel");
+  return SWATTN_OK;
+}
+
+}  // namespace swattn

@@ -33,9 +33,13 @@ def sparse_forward(Q, K, V, sel: BlockSelection, cfg: AttentionConfig,
     if topk.shape[2] != cfg.k_top:
         raise ValueError(f"selection k_top={topk.shape[2]} != cfg.k_top={cfg.k_top}")
     L = _lib.lib()
-    _lib.check(L.swattn_sparse_fwd(_lib.c_config(cfg), Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(),
+    c = _lib.c_config(cfg)
+    from .selection import Workspace
+    ws = Workspace.get(L.swattn_sparse_workspace_bytes(c, n), Qd.device)
+    _lib.check(L.swattn_sparse_fwd(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(),
                                    n, topk.data_ptr(), sel.topk_cnt.data_ptr(), O.data_ptr(),
-                                   lse.data_ptr(), _lib.stream_handle(Qd.device)),
+                                   lse.data_ptr(), ws.data_ptr(), ws.numel(),
+                                   _lib.stream_handle(Qd.device)),
                "swattn_sparse_fwd")
     if counter is not None or stats is not None:
         cnt = sel.topk_cnt.to(torch.int64)

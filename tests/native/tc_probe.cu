@@ -4,6 +4,7 @@
 //   mode 1: A, B K-major SW128, staged by TMA
 //   mode 2: A K-major (TMA), B MN-major SW128 from Bt [128 x N] (TMA)
 //   mode 3: A from TMEM (tcgen05.st), B K-major (TMA)
+//   mode 4: A MN-major SW128 from At [128 x 128] (TMA), B K-major (TMA)
 // Built into tests/native/libtcprobe.so by __graft_entry__.build().
 #include <cuda_bf16.h>
 #include <stdio.h>
@@ -15,7 +16,7 @@ using namespace swattn;
 using namespace swattn::tc;
 
 struct Maps {
-  CUtensorMap a, b, bt;
+  CUtensorMap a, b, bt, at;
 };
 
 __global__ void __launch_bounds__(128) probe_kernel(const __grid_constant__ Maps maps,
@@ -55,7 +56,11 @@ __global__ void __launch_bounds__(128) probe_kernel(const __grid_constant__ Maps
   } else {
     if (threadIdx.x == 0) {
       uint32_t bytes = 0;
-      if (mode != 3) {
+      if (mode == 4) {
+        tma_load_2d(&maps.at, &bar_load, sA, 0, 0);
+        tma_load_2d(&maps.at, &bar_load, sA + 128 * 128, 64, 0);
+        bytes += 32768;
+      } else if (mode != 3) {
         tma_load_2d(&maps.a, &bar_load, sA, 0, 0);
         tma_load_2d(&maps.a, &bar_load, sA + 128 * 128, 64, 0);
         bytes += 32768;
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(128) probe_kernel(const __grid_constant__ Maps
 
   if (warp == 0) {
     if (elect_one()) {
-      const uint32_t id = idesc_bf16(128, N, false, mode == 2);
+      const uint32_t id = idesc_bf16(128, N, mode == 4, mode == 2);
       for (int kk = 0; kk < 8; ++kk) {
         const int h = kk / 4, j = kk % 4;
         uint64_t bdesc;
@@ -101,7 +106,8 @@ __global__ void __launch_bounds__(128) probe_kernel(const __grid_constant__ Maps
         if (mode == 3) {
           mma_ts(tmem, tmem + 256 + kk * 8, bdesc, id, kk > 0);
         } else {
-          const uint64_t adesc = desc_kmajor(smem_u32(sA) + h * 128 * 128 + j * 32);
+          const uint64_t adesc = (mode == 4) ? desc_mnmajor(smem_u32(sA) + kk * 16 * 128, 128 * 128)
+                                             : desc_kmajor(smem_u32(sA) + h * 128 * 128 + j * 32);
           mma_ss(tmem, adesc, bdesc, id, kk > 0);
         }
       }
@@ -123,7 +129,8 @@ __global__ void __launch_bounds__(128) probe_kernel(const __grid_constant__ Maps
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-extern "C" int tc_probe(const void *A, const void *B, const void *Bt, float *D, int N, int mode) {
+extern "C" int tc_probe(const void *A, const void *B, const void *Bt, const void *At, float *D,
+                        int N, int mode) {
   Maps maps;
   uint64_t dimsA[2] = {128, 128}, strA[1] = {256};
   uint32_t boxA[2] = {64, 128};
@@ -134,6 +141,7 @@ extern "C" int tc_probe(const void *A, const void *B, const void *Bt, float *D, 
   uint64_t dimsBt[2] = {(uint64_t)N, 128}, strBt[1] = {(uint64_t)N * 2};
   uint32_t boxBt[2] = {64, 128};
   if (!make_tmap_bf16(&maps.bt, Bt, 2, dimsBt, strBt, boxBt)) return -3;
+  if (!make_tmap_bf16(&maps.at, At, 2, dimsA, strA, boxA)) return -4;
   const int smem = 32768 + 65536 + 1024;
   cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   probe_kernel<<<1, 128, smem>>>(maps, (const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, D, N, mode);

@@ -258,3 +258,20 @@ def test_full_size_properties_and_sampled_rows(n, seed):
     r = torch.as_tensor(rows, device="cuda")
     print(n, "sampled-row sparse err", _tol(res.output[r], want_o, res.lse[r], want_l),
           "reranked rows", int(sel.n_reranked))
+
+
+def test_all_rows_dense_and_forced_sparse_n4096():
+    """Every row (not a sample): at 4K all causal blocks are selected, so the
+    dense kernel and the two-part sparse kernels must both equal dense attention."""
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load("paper_n4096_s0")
+    dense, _ = attend(Qd, Kd, Vd, cfg)
+    sparse, _ = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    torch.cuda.synchronize()
+    want_o, want_l = O.dense_attention(Q, K, V, prof)
+    for res in (dense, sparse):
+        got = res.output.float().cpu().numpy().astype(np.float64)
+        err = np.abs(got - want_o)
+        bad = np.argwhere(err.max(axis=(1, 2)) > O_MAX_ABS).ravel()
+        assert bad.size == 0, f"rows {bad[:10].tolist()} exceed tolerance (max {err.max():.3e})"
+        assert err.mean() <= O_MEAN_ABS
+        assert np.abs(res.lse.cpu().numpy() - want_l).max() <= LSE_ABS
