@@ -1,8 +1,6 @@
 set -x
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 300 python -m pytest tests/test_tc_probe.py -q 2>&1 | tail -5
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -s -k "dense or sparse or attend or determinism or errors" 2>&1 | grep -v "^$" | tail -30
-timeout 300 python __graft_entry__.py smoke 2>&1 | tail -3
-timeout 600 python bench.py --steps 3 --warmup 3 --n 32768 --no-cpu 2>&1 | tail -2
-timeout 900 python bench.py --steps 2 --warmup 3 --n 131072 --no-cpu 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -q -s --timeout 600 2>&1 | grep -E "err|passed|failed|Error|assert|FAIL|max rel|reranked" | head -60
+timeout 600 python tools/diag_scores.py 16384 131072 2>&1 | tail -4
+timeout 900 python bench.py --steps 5 --warmup 3 --n 131072 --no-cpu 2>&1 | tail -2
