@@ -16,6 +16,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxCluster = 256;
+constexpr int kChunk = 128;  // normaliser columns staged per step
 
 struct RerankArgs {
   const __nv_bfloat16 *Q, *kc1, *kc2;
@@ -53,6 +54,8 @@ __device__ double block_reduce_sum(double v, double *red) {
 __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
   __shared__ double q_s[kG][kD];
   __shared__ double lse_s[kG];
+  __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
+  extern __shared__ double kc_s[];  // [kD][kChunk]
   __shared__ double red[kThreads / 32];
   __shared__ int members[kMaxCluster];
   __shared__ double mscore[kMaxCluster];
@@ -74,43 +77,75 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     }
     __syncthreads();
 
-    // ---- pass 1 in float64: lse over the visible normaliser columns
+    // ---- pass 1 in float64: lse over the visible normaliser columns.
+    // 128-column chunks staged as doubles [d][c]; thread = 4 heads x 2 columns
+    // register tile (8 DFMA per 3 shared loads).
     const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
     const int64_t vis2 = a.approx ? vis_count(i, a.l_C2, a.s_C2) : 0;
     const bool use_c2 = a.approx && vis2 > 0;
     const __nv_bfloat16 *kc = use_c2 ? a.kc2 : a.kc1;
     const int64_t vis = use_c2 ? vis2 : vis1;
-    double mloc[kG], lloc[kG];
+    const int hg = threadIdx.x / 64, cg = threadIdx.x % 64;
+    double mloc[4], lloc[4];
 #pragma unroll
-    for (int h = 0; h < kG; ++h) { mloc[h] = -INFINITY; lloc[h] = 0.0; }
-    for (int64_t c = threadIdx.x; c < vis; c += kThreads) {
-      double acc[kG];
-#pragma unroll
-      for (int h = 0; h < kG; ++h) acc[h] = 0.0;
-      const __nv_bfloat16 *kr = kc + (c * a.h_kv + g) * kD;
-      for (int d = 0; d < kD; d += 8) {
-        const uint4 raw = __ldg(reinterpret_cast<const uint4 *>(kr + d));
+    for (int e = 0; e < 4; ++e) { mloc[e] = -INFINITY; lloc[e] = 0.0; }
+    for (int64_t c0 = 0; c0 < vis; c0 += kChunk) {
+      __syncthreads();
+      for (int v = threadIdx.x; v < kChunk * (kD / 8); v += kThreads) {
+        const int c = v % kChunk, d0 = (v / kChunk) * 8;
+        uint4 raw = make_uint4(0, 0, 0, 0);
+        if (c0 + c < vis) raw = __ldg(reinterpret_cast<const uint4 *>(kc + ((c0 + c) * a.h_kv + g) * kD + d0));
         const __nv_bfloat16 *kv = reinterpret_cast<const __nv_bfloat16 *>(&raw);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const double kd = (double)bf2f(kv[e]);
+        for (int e = 0; e < 8; ++e) kc_s[(d0 + e) * kChunk + c] = (double)bf2f(kv[e]);
+      }
+      __syncthreads();
+      double acc[4][2];
 #pragma unroll
-          for (int h = 0; h < kG; ++h) acc[h] = fma(q_s[h][d + e], kd, acc[h]);
+      for (int e = 0; e < 4; ++e) acc[e][0] = acc[e][1] = 0.0;
+#pragma unroll 4
+      for (int d = 0; d < kD; ++d) {
+        const double2 kk = *reinterpret_cast<const double2 *>(&kc_s[d * kChunk + 2 * cg]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double qv = q_s[4 * hg + e][d];
+          acc[e][0] = fma(qv, kk.x, acc[e][0]);
+          acc[e][1] = fma(qv, kk.y, acc[e][1]);
         }
       }
 #pragma unroll
-      for (int h = 0; h < kG; ++h) {
-        const double s = acc[h] * a.scale;
-        if (s > mloc[h]) { lloc[h] = lloc[h] * exp(mloc[h] - s) + 1.0; mloc[h] = s; }
-        else lloc[h] += exp(s - mloc[h]);
+      for (int cc = 0; cc < 2; ++cc) {
+        if (c0 + 2 * cg + cc >= vis) continue;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double sv = acc[e][cc] * a.scale;
+          if (sv > mloc[e]) { lloc[e] = lloc[e] * exp(mloc[e] - sv) + 1.0; mloc[e] = sv; }
+          else lloc[e] += exp(sv - mloc[e]);
+        }
       }
     }
-    for (int h = 0; h < kG; ++h) {
-      const double M = block_reduce_max(mloc[h], red);
-      const double part = (mloc[h] == -INFINITY) ? 0.0 : lloc[h] * exp(mloc[h] - M);
-      const double L = block_reduce_sum(part, red);
-      if (threadIdx.x == 0) lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe
+    // reduce (m, l) over the 64 threads (2 warps) sharing a head group
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double M = mloc[e];
+      for (int o = 16; o; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+      double part = (mloc[e] == -INFINITY) ? 0.0 : lloc[e] * exp(mloc[e] - M);
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if ((threadIdx.x & 31) == 0) {
+        wm[threadIdx.x >> 5][e] = M;
+        wl[threadIdx.x >> 5][e] = part;
+      }
     }
+    __syncthreads();
+    if (threadIdx.x < kG) {
+      const int h = threadIdx.x, w0 = (h / 4) * 2, e = h % 4;
+      const double M = fmax(wm[w0][e], wm[w0 + 1][e]);
+      double L = 0.0;
+      for (int w = w0; w < w0 + 2; ++w)
+        if (wm[w][e] != -INFINITY) L += wl[w][e] * exp(wm[w][e] - M);
+      lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe (selection.py:204)
+    }
+    __syncthreads();
 
     // ---- the boundary cluster from the float32 scores
     const float *src = a.s_cmp + (int64_t)row * a.ld;
@@ -235,7 +270,13 @@ int32_t launch_rerank(const swattn_config *cfg, const void *Q, const void *kc1, 
   a.rows = rows;
   a.cap = cap;
   a.topk = topk;
-  rerank_kernel<<<num_sms * 2, kThreads, 0, stream>>>(a);
+  const size_t smem = (size_t)kD * kChunk * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
   SWATTN_LAUNCH_CHECK("rerank_kernel");
   return SWATTN_OK;
 }

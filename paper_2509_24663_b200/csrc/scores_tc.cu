@@ -64,7 +64,7 @@ struct __align__(1024) ScSmem {
   uint64_t q_full, full[kStages], empty[kStages], tfull[2], tempty[2];
   float2 stat[kRows];          // (m, 1/l) per (token, head) row, log2 domain
   uint32_t edge[4][kTok];      // warp-boundary column values for the max-pool
-  unsigned long long fl[kTok];
+  uint32_t flw[4][kTok];       // per-warp flag bits (16 per warp) per token
   uint32_t tmem_base;
 };
 
@@ -218,7 +218,6 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
 #pragma unroll
         for (int k = 0; k < kTok; ++k) s.edge[quad][k] = __float_as_uint(sc[k]);
       }
-      if (r < kTok) s.fl[r] = 0ull;
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const int qb = r >> 2;                  // block within the tile
       const bool head_lane = (r & 3) == 0 && qb < kTileBlocks;
@@ -234,21 +233,32 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
         if (lane == 28) v4 = __uint_as_float(s.edge[(quad + 1) & 3][k]);
         const float mx = fmaxf(fmaxf(fmaxf(v0, v1), fmaxf(v2, v3)), v4);
         const int64_t tok = i0 + k;
-        if (write && tok < p.n) {
-          p.s_cmp[((int64_t)g * p.n + tok) * p.ld + j] = mx;
-          if (p.flags != nullptr) {
-            const float f = 1.f + 4.f * kScoreRelErr;
-            const bool L = v1 * f < v0 && v2 * f < v0 && v3 * f < v0 && v4 * f < v0;
-            const bool R = v0 * f < v4 && v1 * f < v4 && v2 * f < v4 && v3 * f < v4;
-            const unsigned long long bits =
-                ((unsigned long long)L << (2 * qb)) | ((unsigned long long)R << (2 * qb + 1));
-            if (bits) atomicOr(&s.fl[k], bits);
+        const bool ok = write && tok < p.n;
+        if (ok) p.s_cmp[((int64_t)g * p.n + tok) * p.ld + j] = mx;
+        if (p.flags != nullptr) {
+          // argmax-at-shared-column bits (L: window col 0, R: col 4) with margin
+          const float f = 1.f + 4.f * kScoreRelErr;
+          const bool L = ok && v1 * f < v0 && v2 * f < v0 && v3 * f < v0 && v4 * f < v0;
+          const bool R = ok && v0 * f < v4 && v1 * f < v4 && v2 * f < v4 && v3 * f < v4;
+          const unsigned lm = __ballot_sync(0xffffffffu, L);
+          const unsigned rm = __ballot_sync(0xffffffffu, R);
+          if (lane == 0) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              w |= (((lm >> (4 * e)) & 1u) << (2 * e)) | (((rm >> (4 * e)) & 1u) << (2 * e + 1));
+            s.flw[quad][k] = w;
           }
         }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (p.flags != nullptr && r < kTok && i0 + r < p.n)
-        p.flags[((int64_t)g * p.n + i0 + r) * p.ld_f + t] = s.fl[r];
+      if (p.flags != nullptr && r < kTok && i0 + r < p.n) {
+        const unsigned long long w = (unsigned long long)s.flw[0][r] |
+                                     ((unsigned long long)s.flw[1][r] << 16) |
+                                     ((unsigned long long)s.flw[2][r] << 32) |
+                                     ((unsigned long long)s.flw[3][r] << 48);
+        p.flags[((int64_t)g * p.n + i0 + r) * p.ld_f + t] = w;
+      }
     }
   }
   tc::tc_fence_before();
