@@ -95,8 +95,8 @@ __device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t
 
 __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_constant__ FaParams p) {
   extern __shared__ uint8_t smem_raw[];
-  FaSmem &s = *reinterpret_cast<FaSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                          ~uintptr_t(1023));
+  // align by pointer arithmetic on smem_raw so accesses stay in the shared space
+  FaSmem &s = *reinterpret_cast<FaSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heavy (late) tiles first: causal work grows with the token index
   const int tile = p.n_tiles - 1 - (int)blockIdx.x;

@@ -62,7 +62,7 @@ struct __align__(1024) ScSmem {
   uint8_t q[kQBytes];
   uint8_t k[kStages][kKBytes];
   uint64_t q_full, full[kStages], empty[kStages], tfull[2], tempty[2];
-  float2 stat[kRows];          // (m, 1/l) per (token, head) row, log2 domain
+  __align__(16) float2 stat[kRows];  // (m, 1/l) per (token, head) row, log2 domain
   uint32_t edge[4][kTok];      // warp-boundary column values for the max-pool
   uint32_t flw[4][kTok];       // per-warp flag bits (16 per warp) per token
   uint32_t tmem_base;
@@ -70,8 +70,8 @@ struct __align__(1024) ScSmem {
 
 __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_constant__ ScParams p) {
   extern __shared__ uint8_t smem_raw[];
-  ScSmem &s = *reinterpret_cast<ScSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                          ~uintptr_t(1023));
+  // align by pointer arithmetic on smem_raw so accesses stay in the shared space
+  ScSmem &s = *reinterpret_cast<ScSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heavy CTAs (late tokens) first
   const int tt = p.n_tiles_tok - 1 - (int)blockIdx.x;
@@ -162,25 +162,32 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       tc::tc_fence_after();
       const int64_t c0 = (int64_t)u * kCols;
 #pragma unroll
-      for (int q = 0; q < kCols; q += 32) {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem + lane_off + tb * kCols + q, v);
+      for (int q = 0; q < kCols; q += 64) {
+        uint32_t va[32], vb[32];
+        tc::tmem_ld32(tmem + lane_off + tb * kCols + q, va);
+        tc::tmem_ld32(tmem + lane_off + tb * kCols + q + 32, vb);
         tc::tmem_ld_wait();
-        float x[32];
+        float x[64];
         float cm = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          x[e] = (c0 + q + e < my_vis) ? __uint_as_float(v[e]) * p.scale_log2 : -INFINITY;
+        for (int e = 0; e < 64; ++e) {
+          const uint32_t u = e < 32 ? va[e] : vb[e - 32];
+          x[e] = (c0 + q + e < my_vis) ? __uint_as_float(u) * p.scale_log2 : -INFINITY;
           cm = fmaxf(cm, x[e]);
         }
         if (cm > m) {
           l *= fast_exp2(m - cm);
           m = cm;
         }
-        float acc = 0.f;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) acc += fast_exp2(x[e] - m);
-        if (m != -INFINITY) l += acc;
+        for (int e = 0; e < 64; e += 4) {
+          a0 += fast_exp2(x[e] - m);
+          a1 += fast_exp2(x[e + 1] - m);
+          a2 += fast_exp2(x[e + 2] - m);
+          a3 += fast_exp2(x[e + 3] - m);
+        }
+        if (m != -INFINITY) l += (a0 + a1) + (a2 + a3);
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&s.tempty[tb]);
@@ -189,27 +196,43 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
     asm volatile("bar.sync 1, 128;" ::: "memory");
 
     // ---------------- pass 2: thread = C1 column of the tile
+    int v1k[kTok];
+#pragma unroll
+    for (int k = 0; k < kTok; ++k) v1k[k] = (int)vis_count(i0 + k, p.l_C1, p.s_C1);
     for (int t = 0; t < n_t2; ++t) {
       const int u = n_c1 + t;
       const int tb = u & 1;
-      const int64_t col = (int64_t)t * kTileStride + r;
+      const int col = t * kTileStride + r;
       tc::mbar_wait(&s.tfull[tb], (u >> 1) & 1);
       tc::tc_fence_after();
       float sc[kTok];
 #pragma unroll
-      for (int k = 0; k < kTok; ++k) {
-        uint32_t v[kG];
-        tc::tmem_ld16(tmem + lane_off + tb * kCols + k * kG, v);
+      for (int kb = 0; kb < kTok; kb += 4) {
+        // 4 tokens x 16 heads = 64 TMEM columns per load batch, one wait
+        uint32_t va[32], vb[32];
+        tc::tmem_ld32(tmem + lane_off + tb * kCols + kb * kG, va);
+        tc::tmem_ld32(tmem + lane_off + tb * kCols + kb * kG + 32, vb);
         tc::tmem_ld_wait();
-        float acc = 0.f;
 #pragma unroll
-        for (int h = 0; h < kG; ++h) {
-          const float2 st = s.stat[k * kG + h];
-          acc = fmaf(fast_exp2(fmaf(__uint_as_float(v[h]), p.scale_log2, -st.x)), st.y, acc);
+        for (int k = 0; k < 4; ++k) {
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // independent chains
+#pragma unroll
+          for (int h = 0; h < kG; h += 4) {
+            const int cidx = k * kG + h;
+            const float4 st01 = *reinterpret_cast<const float4 *>(&s.stat[(kb + k) * kG + h]);
+            const float4 st23 = *reinterpret_cast<const float4 *>(&s.stat[(kb + k) * kG + h + 2]);
+            const uint32_t u0 = cidx < 32 ? va[cidx] : vb[cidx - 32];
+            const uint32_t u1 = cidx + 1 < 32 ? va[cidx + 1] : vb[cidx + 1 - 32];
+            const uint32_t u2 = cidx + 2 < 32 ? va[cidx + 2] : vb[cidx + 2 - 32];
+            const uint32_t u3 = cidx + 3 < 32 ? va[cidx + 3] : vb[cidx + 3 - 32];
+            a0 = fmaf(fast_exp2(fmaf(__uint_as_float(u0), p.scale_log2, -st01.x)), st01.y, a0);
+            a1 = fmaf(fast_exp2(fmaf(__uint_as_float(u1), p.scale_log2, -st01.z)), st01.w, a1);
+            a2 = fmaf(fast_exp2(fmaf(__uint_as_float(u2), p.scale_log2, -st23.x)), st23.y, a2);
+            a3 = fmaf(fast_exp2(fmaf(__uint_as_float(u3), p.scale_log2, -st23.z)), st23.w, a3);
+          }
+          const float acc = (a0 + a1) + (a2 + a3);
+          sc[kb + k] = (col >= p.m1) ? -INFINITY : ((col < v1k[kb + k]) ? acc : 0.f);
         }
-        const int64_t tok = i0 + k;
-        const int64_t v1 = vis_count(tok, p.l_C1, p.s_C1);
-        sc[k] = (col >= p.m1) ? -INFINITY : ((col < v1) ? acc : 0.f);
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&s.tempty[tb]);

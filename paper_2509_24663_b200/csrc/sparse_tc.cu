@@ -78,8 +78,8 @@ __device__ __forceinline__ void item_of(const PbParams &p, int64_t it, int &g, i
 
 __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_constant__ PbParams p) {
   extern __shared__ uint8_t smem_raw[];
-  PbSmem &s = *reinterpret_cast<PbSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                          ~uintptr_t(1023));
+  // align by pointer arithmetic on smem_raw so accesses stay in the shared space
+  PbSmem &s = *reinterpret_cast<PbSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {

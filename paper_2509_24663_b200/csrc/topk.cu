@@ -40,6 +40,7 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, in
             int32_t *__restrict__ topk,
             int32_t *__restrict__ topk_cnt, AmbList amb) {
   extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride]
+  __shared__ int hist_s[kWarps * 256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kWarps + warp;  // g * n + i
   if (row >= (int64_t)h_kv * n) return;
@@ -61,15 +62,55 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, in
   for (int t = lane; t < ncand; t += 32) ks[t] = f2key(src[t]);
   __syncwarp();
 
-  // largest T with #(key >= T) >= k  ==  the k-th largest key
-  uint32_t T = 0;
-  for (int bit = 31; bit >= 0; --bit) {
-    const uint32_t cand = T | (1u << bit);
-    int c = 0;
-    for (int t = lane; t < ncand; t += 32) c += ks[t] >= cand;
-    c = __reduce_add_sync(0xffffffffu, c);
-    if (c >= k) T = cand;
+  // k-th largest key T by 4 rounds of 8-bit radix select (warp-private
+  // 256-bin histogram in shared memory, descending scan across lanes)
+  int *hist = hist_s + warp * 256;
+  uint32_t prefix = 0, pmask = 0;
+  int kk = k;  // rank of T among the keys matching the current prefix
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) hist[lane * 8 + e] = 0;
+    __syncwarp();
+    for (int t = lane; t < ncand; t += 32) {
+      const uint32_t v = ks[t];
+      if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1);
+    }
+    __syncwarp();
+    // lane owns bins 255-8*lane .. 248-8*lane (descending)
+    int cnt[8], tot = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      cnt[e] = hist[255 - 8 * lane - e];
+      tot += cnt[e];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - tot;
+    const bool mine = excl < kk && kk <= incl;
+    const unsigned who = __ballot_sync(0xffffffffu, mine);
+    const int src_lane = __ffs(who) - 1;
+    int digit = 0, above = 0;
+    if (mine) {
+      int acc = excl;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (acc + cnt[e] >= kk) { digit = 255 - 8 * lane - e; above = acc; break; }
+        acc += cnt[e];
+      }
+    }
+    digit = __shfl_sync(0xffffffffu, digit, src_lane);
+    above = __shfl_sync(0xffffffffu, above, src_lane);
+    prefix |= (uint32_t)digit << shift;
+    pmask |= 255u << shift;
+    kk -= above;
+    __syncwarp();
   }
+  const uint32_t T = prefix;
   int gt = 0, eq = 0;
   uint32_t below = 0;  // largest key < T
   for (int t = lane; t < ncand; t += 32) {
