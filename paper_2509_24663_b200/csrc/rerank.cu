@@ -8,6 +8,8 @@
 // compression.py:160-173) -- and settles the cluster with the reference's
 // ordering (score desc, index asc; selection.py:125).  Blocks clearly above
 // the cluster stay selected, blocks clearly below stay out.
+#include <string.h>
+
 #include "common.cuh"
 
 namespace swattn {
@@ -30,6 +32,10 @@ struct RerankArgs {
   const int32_t *rows;
   int cap;
   int32_t *topk;
+  // decode rows (seq * h_kv + g): per-sequence Q row, key slabs and length
+  int decode;
+  const int32_t *seq_lens;
+  int64_t max_m1, max_m2;
 };
 
 __device__ double block_reduce_max(double v, double *red) {
@@ -65,15 +71,30 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
   const int total = min(*a.count, a.cap);
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int row = a.rows[item];
-    const int g = row / (int)a.n;
-    const int64_t i = row % a.n;
+    int g;
+    int64_t i, qrow, n_cols = a.n_cols, m1 = a.m1;
+    const __nv_bfloat16 *kc1 = a.kc1, *kc2 = a.kc2;
+    if (a.decode) {
+      const int seq = row / a.h_kv;
+      g = row % a.h_kv;
+      i = a.seq_lens[seq] - 1;
+      qrow = seq;
+      m1 = num_pooled(i + 1, a.l_C1, a.s_C1);
+      n_cols = m1 ? cdiv(m1, a.ps) : 0;
+      kc1 += (int64_t)seq * a.max_m1 * a.h_kv * kD;
+      kc2 += (int64_t)seq * a.max_m2 * a.h_kv * kD;
+    } else {
+      g = row / (int)a.n;
+      i = row % a.n;
+      qrow = i;
+    }
     const int b = (int)(i / a.B);
-    const int hi = cand_hi(b, a.N_local, a.n_cols);
+    const int hi = cand_hi(b, a.N_local, (int)n_cols);
     const int ncand = hi - a.N_init;
     const int k = min(a.k_top, ncand);
     for (int t = threadIdx.x; t < kG * kD; t += kThreads) {
       const int h = t / kD, d = t % kD;
-      q_s[h][d] = (double)bf2f(a.Q[(i * a.h_q + g * kG + h) * kD + d]);
+      q_s[h][d] = (double)bf2f(a.Q[(qrow * a.h_q + g * kG + h) * kD + d]);
     }
     __syncthreads();
 
@@ -83,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
     const int64_t vis2 = a.approx ? vis_count(i, a.l_C2, a.s_C2) : 0;
     const bool use_c2 = a.approx && vis2 > 0;
-    const __nv_bfloat16 *kc = use_c2 ? a.kc2 : a.kc1;
+    const __nv_bfloat16 *kc = use_c2 ? kc2 : kc1;
     const int64_t vis = use_c2 ? vis2 : vis1;
     const int hg = threadIdx.x / 64, cg = threadIdx.x % 64;
     double mloc[4], lloc[4];
@@ -180,10 +201,10 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
       double best = -INFINITY;
       for (int e = 0; e < a.pl; ++e) {
         const int64_t c = (int64_t)j * a.ps + e;
-        if (c >= a.m1) break;
+        if (c >= m1) break;
         double sh = 0.0;
         if (c < vis1) {
-          const __nv_bfloat16 *kr = a.kc1 + (c * a.h_kv + g) * kD;
+          const __nv_bfloat16 *kr = kc1 + (c * a.h_kv + g) * kD;
           for (int h = 0; h < kG; ++h) {
             double dot = 0.0;
             for (int d = lane; d < kD; d += 32) dot = fma(q_s[h][d], (double)bf2f(kr[d]), dot);
@@ -270,6 +291,9 @@ int32_t launch_rerank(const swattn_config *cfg, const void *Q, const void *kc1, 
   a.rows = rows;
   a.cap = cap;
   a.topk = topk;
+  a.decode = 0;
+  a.seq_lens = nullptr;
+  a.max_m1 = a.max_m2 = 0;
   const size_t smem = (size_t)kD * kChunk * sizeof(double);
   static bool attr = false;
   if (!attr) {
@@ -278,6 +302,44 @@ int32_t launch_rerank(const swattn_config *cfg, const void *Q, const void *kc1, 
   }
   rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
   SWATTN_LAUNCH_CHECK("rerank_kernel");
+  return SWATTN_OK;
+}
+
+int32_t launch_rerank_decode(const swattn_config *cfg, const void *q, const void *kc1,
+                             const void *kc2, int max_m1, int max_m2, const int32_t *seq_lens,
+                             int batch, const float *s_cmp, int64_t ld, const int32_t *count,
+                             const int32_t *rows, int32_t cap, int32_t *topk, int num_sms,
+                             cudaStream_t stream) {
+  RerankArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Q = static_cast<const __nv_bfloat16 *>(q);
+  a.kc1 = static_cast<const __nv_bfloat16 *>(kc1);
+  a.kc2 = static_cast<const __nv_bfloat16 *>(kc2);
+  a.s_cmp = s_cmp;
+  a.ld = ld;
+  a.n = 1;
+  a.h_kv = cfg->h_kv;
+  a.h_q = cfg->h_q;
+  a.B = cfg->B;
+  a.N_init = cfg->N_init;
+  a.N_local = cfg->N_local;
+  a.k_top = cfg->k_top;
+  a.l_C1 = cfg->l_C1; a.s_C1 = cfg->s_C1; a.l_C2 = cfg->l_C2; a.s_C2 = cfg->s_C2;
+  a.pl = cfg->l; a.ps = cfg->s;
+  a.approx = 1;
+  a.scale = cfg->scale_compressed_logits ? 1.0 / sqrt((double)cfg->d_h) : 1.0;
+  a.count = count;
+  a.rows = rows;
+  a.cap = cap;
+  a.topk = topk;
+  a.decode = 1;
+  a.seq_lens = seq_lens;
+  a.max_m1 = max_m1;
+  a.max_m2 = max_m2;
+  const size_t smem = (size_t)kD * kChunk * sizeof(double);
+  cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
+  SWATTN_LAUNCH_CHECK("rerank_kernel(decode)");
   return SWATTN_OK;
 }
 

@@ -76,6 +76,13 @@ __device__ __forceinline__ void item_of(const PbParams &p, int64_t it, int &g, i
   t = p.tok0 + it % per;
 }
 
+__device__ __forceinline__ int cnt_of(const PbParams &p, int64_t it) {
+  int g;
+  int64_t t;
+  item_of(p, it, g, t);
+  return p.topk_cnt[(int64_t)g * p.n + t];
+}
+
 __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_constant__ PbParams p) {
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on smem_raw so accesses stay in the shared space
@@ -108,49 +115,76 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (tc::elect_one()) {
+    // Whole warp walks the items; lane l holds block ids l and l+32 of the
+    // current token, fetched one token ahead so no dependent global load sits
+    // between two TMA issues (an L2 round trip per pair halves the gather rate).
+    if (lane == 0) {
       tc::tma_prefetch(&p.q_map);
       tc::tma_prefetch(&p.k_map);
       tc::tma_prefetch(&p.v_map);
-      int64_t pair = 0;
-      int tau = 0;
-      for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+    }
+    int64_t pair = 0;
+    int tau = 0;
+    auto fetch = [&](int64_t item, int &cnt, int &id0, int &id1) {
+      int g;
+      int64_t t;
+      item_of(p, item, g, t);
+      const int64_t row = (int64_t)g * p.n + t;
+      cnt = p.topk_cnt[row];
+      const int32_t *blocks = p.topk + row * p.k_top;
+      id0 = lane < p.k_top ? blocks[lane] : 0;
+      id1 = lane + 32 < p.k_top ? blocks[lane + 32] : 0;
+    };
+    int cnt = 0, id0 = 0, id1 = 0;
+    int64_t it = blockIdx.x;
+    if (it < p.n_items) fetch(it, cnt, id0, id1);
+    while (it < p.n_items) {
+      const int64_t nit = it + gridDim.x;
+      int ncnt = 0, nid0 = 0, nid1 = 0;
+      if (nit < p.n_items) fetch(nit, ncnt, nid0, nid1);
+      if (cnt > 0) {
         int g;
         int64_t t;
         item_of(p, it, g, t);
-        const int64_t row = (int64_t)g * p.n + t;
-        const int cnt = p.topk_cnt[row];
-        if (cnt == 0) continue;
-        const int32_t *blocks = p.topk + row * p.k_top;
         const int qs = tau & 1;
-        tc::mbar_wait(&s.q_empty[qs], ((tau >> 1) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&s.q_full[qs], kQTokBytes);
-        for (int h = 0; h < 2; ++h)
-          tc::tma_load_3d(&p.q_map, &s.q_full[qs], s.q[qs] + h * (kQTokBytes / 2), h * 64, g * kG,
-                          (int)t);
+        if (lane == 0) {
+          tc::mbar_wait(&s.q_empty[qs], ((tau >> 1) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&s.q_full[qs], kQTokBytes);
+          for (int h = 0; h < 2; ++h)
+            tc::tma_load_3d(&p.q_map, &s.q_full[qs], s.q[qs] + h * (kQTokBytes / 2), h * 64,
+                            g * kG, (int)t);
+        }
         const int npairs = (cnt + 1) >> 1;
         for (int pi = 0; pi < npairs; ++pi, ++pair) {
-          const int st = (int)(pair % kStages);
-          const uint32_t ph = ((pair / kStages) & 1) ^ 1;
-          const int b0 = blocks[2 * pi];
-          const int b1 = (2 * pi + 1 < cnt) ? blocks[2 * pi + 1] : b0;  // duplicate: masked
-          tc::mbar_wait(&s.k_empty[st], ph);
-          tc::mbar_arrive_expect_tx(&s.k_full[st], kPairBytes);
-          for (int h = 0; h < 2; ++h) {
-            uint8_t *dst = s.k[st] + h * (kPairBytes / 2);
-            tc::tma_load_2d(&p.k_map, &s.k_full[st], dst, g * kD + h * 64, b0 * kBlk);
-            tc::tma_load_2d(&p.k_map, &s.k_full[st], dst + kBlk * 128, g * kD + h * 64, b1 * kBlk);
+          const int x0 = 2 * pi, x1 = (2 * pi + 1 < cnt) ? 2 * pi + 1 : 2 * pi;  // odd tail: duplicate, masked
+          const int b0 = __shfl_sync(0xffffffffu, x0 < 32 ? id0 : id1, x0 & 31);
+          const int b1 = __shfl_sync(0xffffffffu, x1 < 32 ? id0 : id1, x1 & 31);
+          if (lane == 0) {
+            const int st = (int)(pair % kStages);
+            const uint32_t ph = ((pair / kStages) & 1) ^ 1;
+            tc::mbar_wait(&s.k_empty[st], ph);
+            tc::mbar_arrive_expect_tx(&s.k_full[st], kPairBytes);
+            for (int h = 0; h < 2; ++h) {
+              uint8_t *dst = s.k[st] + h * (kPairBytes / 2);
+              tc::tma_load_2d(&p.k_map, &s.k_full[st], dst, g * kD + h * 64, b0 * kBlk);
+              tc::tma_load_2d(&p.k_map, &s.k_full[st], dst + kBlk * 128, g * kD + h * 64, b1 * kBlk);
+            }
+            tc::mbar_wait(&s.v_empty[st], ph);
+            tc::mbar_arrive_expect_tx(&s.v_full[st], kPairBytes);
+            for (int h = 0; h < 2; ++h) {
+              uint8_t *dst = s.v[st] + h * (kPairBytes / 2);
+              tc::tma_load_2d(&p.v_map, &s.v_full[st], dst, g * kD + h * 64, b0 * kBlk);
+              tc::tma_load_2d(&p.v_map, &s.v_full[st], dst + kBlk * 128, g * kD + h * 64, b1 * kBlk);
+            }
           }
-          tc::mbar_wait(&s.v_empty[st], ph);
-          tc::mbar_arrive_expect_tx(&s.v_full[st], kPairBytes);
-          for (int h = 0; h < 2; ++h) {
-            uint8_t *dst = s.v[st] + h * (kPairBytes / 2);
-            tc::tma_load_2d(&p.v_map, &s.v_full[st], dst, g * kD + h * 64, b0 * kBlk);
-            tc::tma_load_2d(&p.v_map, &s.v_full[st], dst + kBlk * 128, g * kD + h * 64, b1 * kBlk);
-          }
+          __syncwarp();
         }
         ++tau;
       }
+      it = nit;
+      cnt = ncnt;
+      id0 = nid0;
+      id1 = nid1;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -186,11 +220,13 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
       __syncwarp();
       pend = false;
     };
+    int cnt_next = blockIdx.x < p.n_items ? cnt_of(p, blockIdx.x) : 0;
     for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
       int g;
       int64_t t;
       item_of(p, it, g, t);
-      const int cnt = p.topk_cnt[(int64_t)g * p.n + t];
+      const int cnt = cnt_next;  // fetched one item ahead
+      cnt_next = it + gridDim.x < p.n_items ? cnt_of(p, it + gridDim.x) : 0;
       if (cnt == 0) continue;
       const int npairs = (cnt + 1) >> 1;
       const int qs = tau & 1;
@@ -232,12 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     int64_t pair = 0;
     int tau = 0;
+    int cnt_next = blockIdx.x < p.n_items ? cnt_of(p, blockIdx.x) : 0;
     for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
       int g;
       int64_t t;
       item_of(p, it, g, t);
       const int64_t row = (int64_t)g * p.n + t;
-      const int cnt = p.topk_cnt[row];
+      const int cnt = cnt_next;  // fetched one item ahead
+      cnt_next = it + gridDim.x < p.n_items ? cnt_of(p, it + gridDim.x) : 0;
       if (cnt == 0) continue;
       const int npairs = (cnt + 1) >> 1;
       const int64_t ridx = t * p.h_q + g * kG;  // [n][h_q] row of head 0 of the group

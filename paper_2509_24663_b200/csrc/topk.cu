@@ -4,14 +4,15 @@
 // block b is [N_init, min(b - N_local + 1, n_cols)); k = min(k_top, #cand)
 // (0 for rows with no visible pooled entry, :129).  Ranking is score
 // descending with ties to the lower block index -- exactly the stable
-// argsort of :125 -- realised as a radix select on the order-preserving
-// uint32 image of the fp32 score followed by an index-ordered compaction
-// (so the output is already ascending, like np.unique at :133).
+// argsort of :125 -- realised as an 8-bit radix select of the k-th largest
+// order-preserving uint32 image of the fp32 score, followed by an
+// index-ordered compaction (so the output is already ascending, like
+// np.unique at :133).
 //
-// When `amb` is given (select path), rows whose k-th / (k+1)-th boundary is
-// within the float32 error bound of S^cmp are appended to a list for the
+// When an ambiguity list is given (select path), rows whose k-th / (k+1)-th
+// boundary is within the float32 error bound of S^cmp are appended for the
 // float64 re-rank (rerank.cu); exact structural ties (adjacent blocks whose
-// max-pool windows share the argmax column, see scores.cu flags) are not
+// max-pool windows share the argmax column, see scores_tc.cu flags) are not
 // ambiguous and resolve by index exactly as in float64.
 //
 // Roofline: HBM-bound; bytes = candidate S^cmp fp32 read + topk int32 write.
@@ -25,46 +26,29 @@ constexpr int kWarps = 8;
 constexpr int kMaxCand = 4096;  // per-row candidate bound held in smem
 
 struct AmbList {
-  int32_t *count;      // device counter
-  int32_t *rows;       // [cap] packed (g * n + i)
+  int32_t *count;         // device counter
+  int32_t *rows;          // [cap] row ids
   int32_t cap;
-  const uint64_t *flags;  // [h_kv, n, ld_f] or null
+  const uint64_t *flags;  // [rows, ld_f] or null
   int64_t ld_f;
 };
 
-__device__ __forceinline__ int warp_count(bool p) { return __popc(__ballot_sync(0xffffffffu, p)); }
-
-__global__ void __launch_bounds__(kWarps * 32)
-topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, int B,
-            int N_init, int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
-            int32_t *__restrict__ topk,
-            int32_t *__restrict__ topk_cnt, AmbList amb) {
-  extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride]
-  __shared__ int hist_s[kWarps * 256];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;  // g * n + i
-  if (row >= (int64_t)h_kv * n) return;
-  const int64_t i = row % n;
-  const int b = (int)(i / B);
-  const int hi = cand_hi(b, N_local, n_cols);
-  const int ncand = hi > N_init ? hi - N_init : 0;
-  const bool no_visible = (i + 1) < l_C1;
-  const int k = no_visible ? 0 : (ncand < k_top ? ncand : k_top);
-  int32_t *out = topk + row * k_top;
-  if (lane == 0) topk_cnt[row] = k;
-
+// Select the k best of ncand candidate scores src[0..ncand) (block ids
+// N_init + t) into out[0..k_top) ascending (-1 padded).  Warp-cooperative.
+// Returns through the ambiguity list when requested.
+__device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, int N_init,
+                              int k_top, int32_t *__restrict__ out, uint32_t *ks, int *hist,
+                              const AmbList &amb, int64_t row) {
+  const int lane = threadIdx.x & 31;
   if (k == ncand) {  // every candidate is selected (or none)
     for (int t = lane; t < k_top; t += 32) out[t] = t < k ? N_init + t : -1;
     return;
   }
-  const float *src = s_cmp + row * ld + N_init;
-  uint32_t *ks = keys_s + (size_t)warp * cand_stride;
   for (int t = lane; t < ncand; t += 32) ks[t] = f2key(src[t]);
   __syncwarp();
 
-  // k-th largest key T by 4 rounds of 8-bit radix select (warp-private
-  // 256-bin histogram in shared memory, descending scan across lanes)
-  int *hist = hist_s + warp * 256;
+  // k-th largest key T: 4 rounds of 8-bit radix select (warp-private
+  // 256-bin histogram, descending scan across lanes)
   uint32_t prefix = 0, pmask = 0;
   int kk = k;  // rank of T among the keys matching the current prefix
 #pragma unroll 1
@@ -77,8 +61,7 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, in
       if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1);
     }
     __syncwarp();
-    // lane owns bins 255-8*lane .. 248-8*lane (descending)
-    int cnt[8], tot = 0;
+    int cnt[8], tot = 0;  // lane owns bins 255-8*lane .. 248-8*lane (descending)
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       cnt[e] = hist[255 - 8 * lane - e];
@@ -92,14 +75,17 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, in
     }
     const int excl = incl - tot;
     const bool mine = excl < kk && kk <= incl;
-    const unsigned who = __ballot_sync(0xffffffffu, mine);
-    const int src_lane = __ffs(who) - 1;
+    const int src_lane = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
     int digit = 0, above = 0;
     if (mine) {
       int acc = excl;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        if (acc + cnt[e] >= kk) { digit = 255 - 8 * lane - e; above = acc; break; }
+        if (acc + cnt[e] >= kk) {
+          digit = 255 - 8 * lane - e;
+          above = acc;
+          break;
+        }
         acc += cnt[e];
       }
     }
@@ -179,6 +165,49 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, in
   }
 }
 
+__global__ void __launch_bounds__(kWarps * 32)
+topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, int B, int N_init,
+            int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
+            int32_t *__restrict__ topk, int32_t *__restrict__ topk_cnt, AmbList amb) {
+  extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride]
+  __shared__ int hist_s[kWarps * 256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;  // g * n + i
+  if (row >= (int64_t)h_kv * n) return;
+  const int64_t i = row % n;
+  const int b = (int)(i / B);
+  const int hi = cand_hi(b, N_local, n_cols);
+  const int ncand = hi > N_init ? hi - N_init : 0;
+  const bool no_visible = (i + 1) < l_C1;
+  const int k = no_visible ? 0 : (ncand < k_top ? ncand : k_top);
+  if (lane == 0) topk_cnt[row] = k;
+  warp_topk_row(s_cmp + row * ld + N_init, ncand, k, N_init, k_top, topk + row * k_top,
+                keys_s + (size_t)warp * cand_stride, hist_s + warp * 256, amb, row);
+}
+
+// decode: row = (seq b, group g); the query position is seq_lens[b]-1
+__global__ void __launch_bounds__(kWarps * 32)
+decode_topk_kernel(const float *__restrict__ s_cmp, int64_t ld, const int32_t *__restrict__ seq_lens,
+                   int batch, int h_kv, int B, int N_init, int N_local, int k_top, int l_C1, int s_C1,
+                   int pool_s, int cand_stride, int32_t *__restrict__ topk,
+                   int32_t *__restrict__ topk_cnt, AmbList amb) {
+  extern __shared__ uint32_t keys_s[];
+  __shared__ int hist_s[kWarps * 256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;  // seq * h_kv + g
+  if (row >= (int64_t)batch * h_kv) return;
+  const int L = seq_lens[row / h_kv];
+  const int64_t i = L - 1;
+  const int64_t m1 = num_pooled(L, l_C1, s_C1);
+  const int n_cols = (int)(m1 ? cdiv(m1, pool_s) : 0);
+  const int hi = cand_hi((int)(i / B), N_local, n_cols);
+  const int ncand = hi > N_init ? hi - N_init : 0;
+  const int k = (i + 1) < l_C1 ? 0 : min(ncand, k_top);
+  if (lane == 0) topk_cnt[row] = k;
+  warp_topk_row(s_cmp + row * ld + N_init, ncand, k, N_init, k_top, topk + row * k_top,
+                keys_s + (size_t)warp * cand_stride, hist_s + warp * 256, amb, row);
+}
+
 }  // namespace
 
 int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, int64_t n,
@@ -195,12 +224,37 @@ int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, in
   AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
   const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
   const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
-  if (smem > 48 * 1024)
+  if (smem > 40 * 1024)
     cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   topk_kernel<<<(unsigned)cdiv(rows, kWarps), kWarps * 32, smem, stream>>>(
       s_cmp, ld, n, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols, cfg->l_C1,
       cand_stride, topk, topk_cnt, amb);
   SWATTN_LAUNCH_CHECK("topk_kernel");
+  return SWATTN_OK;
+}
+
+int32_t launch_decode_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld,
+                           const int32_t *seq_lens, int batch, int max_ctx, int32_t *topk,
+                           int32_t *topk_cnt, int32_t *amb_count, int32_t *amb_rows,
+                           int32_t amb_cap, cudaStream_t stream) {
+  const int64_t m1 = num_pooled(max_ctx, cfg->l_C1, cfg->s_C1);
+  const int n_cols = (int)(m1 ? cdiv(m1, cfg->s) : 0);
+  if (n_cols - cfg->N_init > kMaxCand) {
+    set_error("unsupported: %d top-k candidates exceed the compiled bound %d", n_cols, kMaxCand);
+    return SWATTN_EUNSUPPORTED;
+  }
+  if (cfg->k_top <= 0) return SWATTN_OK;
+  const int64_t rows = (int64_t)cfg->h_kv * batch;
+  AmbList amb{amb_count, amb_rows, amb_cap, nullptr, 0};
+  const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
+  const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
+  if (smem > 40 * 1024)
+    cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  decode_topk_kernel<<<(unsigned)cdiv(rows, kWarps), kWarps * 32, smem, stream>>>(
+      s_cmp, ld, seq_lens, batch, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top,
+      cfg->l_C1, cfg->s_C1, cfg->s, cand_stride, topk, topk_cnt, amb);
+  SWATTN_LAUNCH_CHECK("decode_topk_kernel");
   return SWATTN_OK;
 }
 

@@ -275,3 +275,45 @@ def test_all_rows_dense_and_forced_sparse_n4096():
         assert bad.size == 0, f"rows {bad[:10].tolist()} exceed tolerance (max {err.max():.3e})"
         assert err.mean() <= O_MEAN_ABS
         assert np.abs(res.lse.cpu().numpy() - want_l).max() <= LSE_ABS
+
+
+def test_decode_paged_matches_oracle_last_row():
+    """K6 decode over a shuffled paged cache == row L-1 of the reference's
+    sparse path (selection bit-exact, output within tolerance)."""
+    from paper_2509_24663_b200.decode import PagedKVCache, decode_step
+    prof, cfg = O.PAPER, AttentionConfig()
+    lens = [9000, 12345, 20000]
+    data = [O.draw_qkv(L, 32, 2, 128, 40 + b) for b, L in enumerate(lens)]
+    cache = PagedKVCache(cfg, batch=len(lens), max_pages=-(-max(lens) // 64) + 2, seed=5)
+    for b, (Q, K, V) in enumerate(data):
+        cache.append(b, _dev(K), _dev(V))
+    q = torch.stack([_dev(Q[L - 1]) for (Q, K, V), L in zip(data, lens)])
+    res, topk = decode_step(cache, q, return_topk=True)
+    torch.cuda.synchronize()
+    for b, ((Q, K, V), L) in enumerate(zip(data, lens)):
+        o, l, top = O.decode_row(Q[L - 1], K, V, L - 1, prof)
+        assert np.array_equal(topk[b].cpu().numpy(), top), b
+        err = np.abs(res.output[b].float().cpu().numpy() - o)
+        assert err.max() <= O_MAX_ABS and err.mean() <= O_MEAN_ABS, (b, err.max())
+        assert np.abs(res.lse[b].cpu().numpy() - l).max() <= LSE_ABS
+    # pooled-key slabs equal the one-shot K1 pooling of the whole context
+    for b, ((Q, K, V), L) in enumerate(zip(data, lens)):
+        c1 = O.pool(K, 32, 16)
+        got = cache.kc1[b, :c1.shape[0]].contiguous().view(torch.int16).cpu().numpy()
+        assert np.array_equal(got, c1.view(np.int16))
+
+
+def test_decode_incremental_append_equals_bulk():
+    """Appending token by token keeps the compressed keys identical to a
+    bulk append (windows completing at 16/64-token boundaries)."""
+    from paper_2509_24663_b200.decode import PagedKVCache
+    cfg = AttentionConfig()
+    Q, K, V = O.draw_qkv(700, 32, 2, 128, 77)
+    a = PagedKVCache(cfg, batch=1, max_pages=12, seed=1)
+    b = PagedKVCache(cfg, batch=1, max_pages=12, seed=2)
+    a.append(0, _dev(K), _dev(V))
+    b.append(0, _dev(K[:500]), _dev(V[:500]))
+    for t in range(500, 700):
+        b.append(0, _dev(K[t:t + 1]), _dev(V[t:t + 1]))
+    torch.cuda.synchronize()
+    assert torch.equal(a.kc1, b.kc1) and torch.equal(a.kc2, b.kc2)

@@ -31,7 +31,10 @@ __global__ void __launch_bounds__(128) gather_kernel(const __grid_constant__ CUt
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   __shared__ uint64_t full[32];
+  __shared__ int ids_s[2048];
   const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < iters && i < 2048; i += blockDim.x)
+    ids_s[i] = ids[(blockIdx.x * iters + i) & 0xFFFFF];
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
@@ -42,7 +45,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const __grid_constant__ CUt
     unsigned long long acc = 0;
     for (int it = 0; it < iters; ++it) {
       const int st = it % stages;
-      const int id = ids[(blockIdx.x * iters + it) & 0xFFFFF];
+      const int id = ids_s[it & 2047];
       const uint8_t *src = base + (size_t)id * kTile;
       for (int v = threadIdx.x; v < kTile / 16; v += 128) {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + st * kTile + v * 16)),
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const __grid_constant__ CUt
       }
       if (it < iters) {
         const int st = it % stages;
-        const int id = ids[(blockIdx.x * iters + it) & 0xFFFFF];
+        const int id = ids_s[it & 2047];
         mbar_arrive_expect_tx(&full[st], kTile);
         if (kMode == 0) {
           // 2D TMA box {64 elems, 64 rows} from a [rows][256 elems] tensor (row stride 512 B)
