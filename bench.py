@@ -287,8 +287,9 @@ def run_ours(args):
             "dense_comparator": dense,
             "clocks": clk.summary(),
         }
-        if dense.get("ms"):
-            line["speedup_vs_dense"] = dense["ms"] / ms
+        if dense.get("best"):
+            line["speedup_vs_dense"] = dense["best"]["ms"] / ms
+            line["speedup_vs_dense_impl"] = dense["best"]["impl"]
         if not args.no_cpu and ws == 1:
             line["cpu_baseline"] = cpu_baseline_sample(n, rows_n=args.cpu_rows)
         print(json.dumps(line), flush=True)
@@ -363,38 +364,58 @@ def stage_breakdown(L, c, cfg, Q, K, V, n, stream, reps=2):
     return out
 
 
-def dense_comparator(Q, K, V, cfg, n, stream):
-    """Dense causal GQA flash attention of the same shape (library kernel)."""
+def dense_comparator(Q, K, V, cfg, n, stream, reps=3):
+    """Dense causal GQA attention of the same shape: our own tcgen05 K5 and
+    every library kernel in the image that runs it; `best` is the fastest."""
     import torch
-    res = {}
+    import torch.nn.functional as F
+    from paper_2509_24663_b200 import _lib
+    from paper_2509_24663_b200.counts import dense_total_counts
+
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    O_ = torch.empty_like(Q)
+    lse = torch.empty((n, 32), dtype=torch.float32, device="cuda")
+    cands = {"own K5 tcgen05 (swattn_dense_fwd)": lambda: _lib.check(L.swattn_dense_fwd(
+        c, Q.data_ptr(), K.data_ptr(), V.data_ptr(), n, 1, O_.data_ptr(), lse.data_ptr(),
+        stream.cuda_stream), "dense")}
     try:
         from flash_attn import flash_attn_func
-        fn = lambda: flash_attn_func(Q[None], K[None], V[None], causal=True)
-        name = "flash_attn 2.8.3 (FA2, sm_100 build)"
+        cands["flash_attn 2.8.3 (FA2 sm_100 build)"] = lambda: flash_attn_func(
+            Q[None], K[None], V[None], causal=True)
     except Exception:
-        import torch.nn.functional as F
-        q = Q.transpose(0, 1)[None]
-        k = K.transpose(0, 1)[None]
-        v = V.transpose(0, 1)[None]
-        fn = lambda: F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
-        name = "torch SDPA"
-    try:
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        reps = 3
-        for _ in range(reps):
+        pass
+    q = Q.transpose(0, 1)[None]
+    k = K.transpose(0, 1).repeat_interleave(16, dim=0)[None]
+    v = V.transpose(0, 1).repeat_interleave(16, dim=0)[None]
+
+    def cudnn():
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+            return F.scaled_dot_product_attention(q, k, v, is_causal=True)
+    cands["torch SDPA cuDNN"] = cudnn
+    mac, _ = dense_total_counts(cfg, n)
+    out = {}
+    for name, fn in cands.items():
+        try:
             fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / reps
-        from paper_2509_24663_b200.counts import dense_total_counts
-        mac, _ = dense_total_counts(cfg, n)
-        res = {"impl": name, "ms": ms, "tflops": 2 * mac / (ms / 1e3) / 1e12}
-    except Exception as e:  # pragma: no cover
-        res = {"impl": name, "error": str(e)[:200]}
-    return res
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            out[name] = {"ms": ms, "tflops": 2 * mac / (ms / 1e3) / 1e12}
+        except Exception as e:  # pragma: no cover - comparator unavailable
+            out[name] = {"error": str(e)[:160]}
+    del k, v
+    ok = {kk: vv for kk, vv in out.items() if "ms" in vv}
+    if ok:
+        best = min(ok, key=lambda kk: ok[kk]["ms"])
+        out["best"] = {"impl": best, "ms": ok[best]["ms"]}
+    return out
 
 
 def main():

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const __grid_constant__ CUt
   for (int i = threadIdx.x; i < iters && i < 2048; i += blockDim.x)
     ids_s[i] = ids[(blockIdx.x * iters + i) & 0xFFFFF];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < stages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < 32; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -60,6 +60,31 @@ __global__ void __launch_bounds__(128) gather_kernel(const __grid_constant__ CUt
     __syncthreads();
     acc += smem[threadIdx.x];
     if (threadIdx.x == 0) atomicAdd(sink, acc);
+    return;
+  }
+  if (kMode == 3) {
+    // 4 producer warps, each with its own ring of stages/4 slots
+    const int ring = stages / 4;
+    uint8_t *mine = smem + warp * ring * kTile;
+    uint64_t *bars = full + warp * 8;
+    if (elect_one()) {
+      const int per = iters / 4;
+      for (int it = 0; it < per + ring; ++it) {
+        if (it >= ring) {
+          const int c = it - ring;
+          mbar_wait(&bars[c % ring], (c / ring) & 1);
+        }
+        if (it < per) {
+          const int st = it % ring;
+          const int id = ids_s[(warp * per + it) & 2047];
+          mbar_arrive_expect_tx(&bars[st], kTile);
+          tma_load_2d(&map, &bars[st], mine + st * kTile, (id & 1) * 128 + ((id >> 1) & 1) * 64,
+                      (id >> 2) * 64);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(sink, (unsigned long long)smem[5]);
     return;
   }
   if (warp == 0 && elect_one()) {
@@ -112,16 +137,17 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int iters = 2048;
-  const char *names[3] = {"TMA 2D box 64x128B (strided rows)", "cp.async.bulk 8 KB contiguous",
-                          "LDGSTS 16 B x 512 per tile"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char *names[4] = {"TMA 2D box 64x128B (strided rows)", "cp.async.bulk 8 KB contiguous",
+                          "LDGSTS 16 B x 512 per tile", "TMA, 4 producer warps"};
+  for (int mode = 0; mode < 4; ++mode) {
     for (int stages : {4, 8, 16, 24}) {
-      for (int cpsm : {1, 2}) {
+      for (int cpsm : {1, 2, 3, 4}) {
         const int smem = stages * kTile + 1024;
         if (smem * cpsm > 220 * 1024) continue;
         if (mode == 2 && stages < 8) continue;
+        if (mode == 3 && stages < 8) continue;
         void (*k)(CUtensorMap, const uint8_t *, const int *, int, int, unsigned long long *) =
-            mode == 0 ? gather_kernel<0> : mode == 1 ? gather_kernel<1> : gather_kernel<2>;
+            mode == 0 ? gather_kernel<0> : mode == 1 ? gather_kernel<1> : mode == 2 ? gather_kernel<2> : gather_kernel<3>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         const int grid = sms * cpsm;
         k<<<grid, 128, smem>>>(map, base, ids, 64, stages, sink);

@@ -1,9 +1,4 @@
 set -x
-mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 2>&1 | tail -3
-timeout 300 ./tools/gather_bench 2>&1 | tee gpurun_out/gather_bench.txt
-K='regex:compress|scores|topk|rerank|fa_tile|sparse_pb|attention_list'
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv --log-file gpurun_out/launches_128k.csv python tools/one_attend.py 131072 > /dev/null 2>&1
-grep -v "^==" gpurun_out/launches_128k.csv | awk -F'","' '{print $5, $NF}' | sed 's/"//g' | tail -8
+timeout 300 ./tools/gather_bench 2>&1 | tee gpurun_out/gather_bench3.txt
 timeout 900 python bench.py --steps 5 --warmup 3 --n 131072 --no-cpu 2>&1 | tail -1
