@@ -9,8 +9,9 @@
 //   query block shares, selection.py:113-119): [0, n_init) U [lo, b].
 //
 // Warp roles (192 threads, 2 CTAs / SM):
-//   warp 0      TMA producer: Q once, then K and V blocks through two
-//               independent 2-stage rings (K freed after QK^T, V after PV);
+//   warp 0      TMA producers: lane 0 issues Q once then K blocks, lane 1
+//               V blocks, through two independent 2-stage rings (K freed
+//               after QK^T, V after PV);
 //   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into a
 //               double-buffered TMEM S tile (128 x 64 fp32), then
 //               O += P_{j-1} V_{j-1} with P read straight from TMEM (kind::f16
@@ -131,11 +132,12 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
   const uint32_t tmem_o = tmem + 128;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (tc::elect_one()) {
+    // ------------------------------------------------------------ TMA producers
+    // lane 0: Q + K blocks, lane 1: V blocks -- two issuing threads, since one
+    // thread's TMA issue rate caps near 36 GB/s (tools/gather_bench.cu)
+    if (lane == 0) {
       tc::tma_prefetch(&p.q_map);
       tc::tma_prefetch(&p.k_map);
-      tc::tma_prefetch(&p.v_map);
       tc::mbar_arrive_expect_tx(&s.q_full, kQBytes);
       for (int h = 0; h < 2; ++h)
         tc::tma_load_3d(&p.q_map, &s.q_full, s.q + h * (kQBytes / 2), h * 64, g * kG, (int)t0);
@@ -148,6 +150,13 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         for (int h = 0; h < 2; ++h)
           tc::tma_load_2d(&p.k_map, &s.k_full[st], s.k[st] + h * (kKVBytes / 2), g * kD + h * 64,
                           key0);
+      }
+    } else if (lane == 1) {
+      tc::tma_prefetch(&p.v_map);
+      for (int i = 0; i < nblk; ++i) {
+        const int st = i % kStages;
+        const uint32_t ph = ((i / kStages) & 1) ^ 1;
+        const int key0 = L.at(i) * kBlk;
         tc::mbar_wait(&s.v_empty[st], ph);
         tc::mbar_arrive_expect_tx(&s.v_full[st], kKVBytes);
         for (int h = 0; h < 2; ++h)
@@ -155,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
                           key0);
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id_s = tc::idesc_bf16(kRows, kBlk, false, false);

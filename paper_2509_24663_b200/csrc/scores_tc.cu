@@ -105,14 +105,18 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
   const uint32_t tmem = s.tmem_base;
 
   if (warp == 0) {
-    if (tc::elect_one()) {
-      tc::tma_prefetch(&p.q_map);
-      tc::tma_prefetch(&p.k1_map);
-      tc::tma_prefetch(&p.k2_map);
-      tc::mbar_arrive_expect_tx(&s.q_full, kQBytes);
-      for (int h = 0; h < 2; ++h)
-        tc::tma_load_3d(&p.q_map, &s.q_full, s.q + h * (kQBytes / 2), h * 64, g * kG, (int)i0);
-      for (int u = 0; u < n_units; ++u) {
+    // lanes 0 and 1 each own one ring stage (units u = lane mod 2): two issuing
+    // threads, since one thread's TMA issue rate caps near 36 GB/s
+    if (lane < kStages) {
+      if (lane == 0) {
+        tc::tma_prefetch(&p.q_map);
+        tc::tma_prefetch(&p.k1_map);
+        tc::tma_prefetch(&p.k2_map);
+        tc::mbar_arrive_expect_tx(&s.q_full, kQBytes);
+        for (int h = 0; h < 2; ++h)
+          tc::tma_load_3d(&p.q_map, &s.q_full, s.q + h * (kQBytes / 2), h * 64, g * kG, (int)i0);
+      }
+      for (int u = lane; u < n_units; u += kStages) {
         const int st = u % kStages;
         tc::mbar_wait(&s.empty[st], ((u / kStages) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&s.full[st], kKBytes);
@@ -123,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
           tc::tma_load_2d(map, &s.full[st], s.k[st] + h * (kKBytes / 2), g * kD + h * 64, row0);
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     const uint32_t idesc = tc::idesc_bf16(128, 128, false, false);
     const uint32_t q_addr = tc::smem_u32(s.q);

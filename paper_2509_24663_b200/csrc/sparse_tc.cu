@@ -17,9 +17,11 @@
 // sparse_forward (sparse.py:70-91).  A token whose logits exceed m_A by more
 // than 2^64 is listed for the CUDA-core exact path (never on sane inputs).
 //
-// Warp roles (192 threads, 1 CTA / SM, persistent over (group, token)):
-//   warp 0 TMA producer (Q_t, K/V pairs, 3-stage rings), warp 1 MMA issuer,
-//   warps 2..5 softmax + per-token epilogue.
+// Warp roles (256 threads, 1 CTA / SM, persistent over (group, token)):
+//   warps 0..2 TMA producers -- warp w owns ring stage w (pairs p = w mod 3):
+//              a single issuing thread tops out near 36 GB/s of TMA traffic
+//              (tools/gather_bench.cu), so the gather needs several issuers;
+//   warp 3     MMA issuer; warps 4..7 softmax + per-token epilogue.
 // Roofline: bound by the L2->SMEM gather of 2 x 63 x 16 KB per token
 // (K and V of the selected blocks); FLOP = 4 * 16 * 64 * d per block.
 #include <string.h>
@@ -32,7 +34,8 @@ namespace swattn {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;
+constexpr int kMmaWarp = 3;  // warps [0, kStages) produce, then MMA, then 4 softmax warps
 constexpr int kStages = 3;
 constexpr int kBlk = 64;
 constexpr uint32_t kPairBytes = 2 * kBlk * kD * 2;  // 32 KB (K or V of two blocks)
@@ -107,14 +110,14 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
     }
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc<kTmemCols>(&s.tmem_base);
+  if (warp == kMmaWarp) tc::tmem_alloc<kTmemCols>(&s.tmem_base);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = s.tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp < kStages) {
+    // ------------------------------------------------------------ TMA producers
     // Whole warp walks the items; lane l holds block ids l and l+32 of the
     // current token, fetched one token ahead so no dependent global load sits
     // between two TMA issues (an L2 round trip per pair halves the gather rate).
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
         int64_t t;
         item_of(p, it, g, t);
         const int qs = tau & 1;
-        if (lane == 0) {
+        if (lane == 0 && warp == 0) {
           tc::mbar_wait(&s.q_empty[qs], ((tau >> 1) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&s.q_full[qs], kQTokBytes);
           for (int h = 0; h < 2; ++h)
@@ -159,8 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
           const int x0 = 2 * pi, x1 = (2 * pi + 1 < cnt) ? 2 * pi + 1 : 2 * pi;  // odd tail: duplicate, masked
           const int b0 = __shfl_sync(0xffffffffu, x0 < 32 ? id0 : id1, x0 & 31);
           const int b1 = __shfl_sync(0xffffffffu, x1 < 32 ? id0 : id1, x1 & 31);
-          if (lane == 0) {
-            const int st = (int)(pair % kStages);
+          if (lane == 0 && (int)(pair % kStages) == warp) {
+            const int st = warp;
             const uint32_t ph = ((pair / kStages) & 1) ^ 1;
             tc::mbar_wait(&s.k_empty[st], ph);
             tc::mbar_arrive_expect_tx(&s.k_full[st], kPairBytes);
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
       id0 = nid0;
       id1 = nid1;
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id_s = tc::idesc_bf16(128, kG, false, false);
     const uint32_t id_o = tc::idesc_bf16(128, kG, true, false);
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
+  if (warp == kMmaWarp) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
 }  // namespace

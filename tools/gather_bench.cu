@@ -62,12 +62,16 @@ __global__ void __launch_bounds__(128) gather_kernel(const __grid_constant__ CUt
     if (threadIdx.x == 0) atomicAdd(sink, acc);
     return;
   }
-  if (kMode == 3) {
-    // 4 producer warps, each with its own ring of stages/4 slots
+  if (kMode == 3 || kMode == 4) {
+    // 4 issuers, each with its own ring of stages/4 slots: mode 3 = one
+    // elected lane in each of 4 warps, mode 4 = lanes 0..3 of warp 0
     const int ring = stages / 4;
-    uint8_t *mine = smem + warp * ring * kTile;
-    uint64_t *bars = full + warp * 8;
-    if (elect_one()) {
+    const int who = kMode == 3 ? warp : (threadIdx.x & 31);
+    uint8_t *mine = smem + who * ring * kTile;
+    uint64_t *bars = full + who * 8;
+    const bool issuer = kMode == 3 ? elect_one() : (warp == 0 && who < 4);
+    if (issuer) {
+      const int warp = who;
       const int per = iters / 4;
       for (int it = 0; it < per + ring; ++it) {
         if (it >= ring) {
@@ -137,17 +141,19 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int iters = 2048;
-  const char *names[4] = {"TMA 2D box 64x128B (strided rows)", "cp.async.bulk 8 KB contiguous",
-                          "LDGSTS 16 B x 512 per tile", "TMA, 4 producer warps"};
-  for (int mode = 0; mode < 4; ++mode) {
+  const char *names[5] = {"TMA 2D box 64x128B (strided rows)", "cp.async.bulk 8 KB contiguous",
+                          "LDGSTS 16 B x 512 per tile", "TMA, 4 producer warps",
+                          "TMA, 4 producer lanes of 1 warp"};
+  for (int mode = 0; mode < 5; ++mode) {
     for (int stages : {4, 8, 16, 24}) {
       for (int cpsm : {1, 2, 3, 4}) {
         const int smem = stages * kTile + 1024;
         if (smem * cpsm > 220 * 1024) continue;
         if (mode == 2 && stages < 8) continue;
-        if (mode == 3 && stages < 8) continue;
+        if (mode >= 3 && stages < 8) continue;
+        if (mode < 3 && stages > 8) continue;
         void (*k)(CUtensorMap, const uint8_t *, const int *, int, int, unsigned long long *) =
-            mode == 0 ? gather_kernel<0> : mode == 1 ? gather_kernel<1> : mode == 2 ? gather_kernel<2> : gather_kernel<3>;
+            mode == 0 ? gather_kernel<0> : mode == 1 ? gather_kernel<1> : mode == 2 ? gather_kernel<2> : mode == 3 ? gather_kernel<3> : gather_kernel<4>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         const int grid = sms * cpsm;
         k<<<grid, 128, smem>>>(map, base, ids, 64, stages, sink);
