@@ -47,19 +47,39 @@ __device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, i
   for (int t = lane; t < ncand; t += 32) ks[t] = f2key(src[t]);
   __syncwarp();
 
-  // k-th largest key T: 4 rounds of 8-bit radix select (warp-private
-  // 256-bin histogram, descending scan across lanes)
-  uint32_t prefix = 0, pmask = 0;
+  // k-th largest key T: rounds of 8-bit radix select (warp-private 256-bin
+  // histogram, descending scan across lanes).  The bits every key shares
+  // (scores live in a narrow positive range) are skipped, and lanes that hit
+  // the same bin aggregate into one shared-memory atomic.
+  uint32_t kmin = 0xffffffffu, kmax = 0;
+  for (int t = lane; t < ncand; t += 32) {
+    kmin = min(kmin, ks[t]);
+    kmax = max(kmax, ks[t]);
+  }
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  const int common = (kmin == kmax) ? 32 : __clz(kmin ^ kmax);  // shared leading bits
+  uint32_t pmask = common >= 32 ? 0xffffffffu : ~(0xffffffffu >> common);
+  uint32_t prefix = kmin & pmask;
   int kk = k;  // rank of T among the keys matching the current prefix
 #pragma unroll 1
-  for (int shift = 24; shift >= 0; shift -= 8) {
+  for (int shift = 32 - common - 8; shift > -8; shift -= 8) {
+    const int sh = shift < 0 ? 0 : shift;  // last round may overlap matched bits
 #pragma unroll
     for (int e = 0; e < 8; ++e) hist[lane * 8 + e] = 0;
     __syncwarp();
-    for (int t = lane; t < ncand; t += 32) {
-      const uint32_t v = ks[t];
-      if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1);
+    for (int base = 0; base < ncand; base += 32) {
+      const int t = base + lane;
+      const uint32_t v = t < ncand ? ks[t] : 0u;
+      const bool ok = t < ncand && (v & pmask) == prefix;
+      const unsigned act = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        const uint32_t bin = (v >> sh) & 255u;
+        const unsigned same = __match_any_sync(act, bin);
+        if ((__ffs(same) - 1) == lane) atomicAdd(&hist[bin], __popc(same));
+      }
     }
+    __syncwarp();
     __syncwarp();
     int cnt[8], tot = 0;  // lane owns bins 255-8*lane .. 248-8*lane (descending)
 #pragma unroll
@@ -91,8 +111,8 @@ __device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, i
     }
     digit = __shfl_sync(0xffffffffu, digit, src_lane);
     above = __shfl_sync(0xffffffffu, above, src_lane);
-    prefix |= (uint32_t)digit << shift;
-    pmask |= 255u << shift;
+    prefix |= (uint32_t)digit << sh;
+    pmask |= 255u << sh;
     kk -= above;
     __syncwarp();
   }

@@ -1,8 +1,4 @@
 set -x
 export PYTHONUNBUFFERED=1
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 2>&1 | grep -E "passed|failed|Error|assert|FAIL" | head -20
-timeout 300 ./tools/gather_bench 2>&1 | grep -E "producer" | tee gpurun_out/gather_bench4.txt
-K='regex:compress|scores|topk|rerank|fa_tile|sparse_pb|attention_list'
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv --log-file gpurun_out/launches_128k.csv python tools/one_attend.py 131072 > /dev/null 2>&1
-grep -v "^==" gpurun_out/launches_128k.csv | awk -F'","' '{print $5, $NF}' | sed 's/"//g' | tail -8
-timeout 900 python bench.py --steps 5 --warmup 3 --n 131072 --no-cpu 2>&1 | tail -1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_pb -s 1 -c 1 -o gpurun_out/prof_pb2 python tools/one_attend.py 131072 > gpurun_out/ncu_pb2.log 2>&1; tail -2 gpurun_out/ncu_pb2.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:scores_tc -s 1 -c 1 -o gpurun_out/prof_sc2 python tools/one_attend.py 131072 > gpurun_out/ncu_sc2.log 2>&1; tail -2 gpurun_out/ncu_sc2.log
