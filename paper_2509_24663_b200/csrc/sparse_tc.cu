@@ -17,11 +17,12 @@
 // sparse_forward (sparse.py:70-91).  A token whose logits exceed m_A by more
 // than 2^64 is listed for the CUDA-core exact path (never on sane inputs).
 //
-// Warp roles (256 threads, 1 CTA / SM, persistent over (group, token)):
-//   warps 0..2 TMA producers -- warp w owns ring stage w (pairs p = w mod 3):
-//              a single issuing thread tops out near 36 GB/s of TMA traffic
-//              (tools/gather_bench.cu), so the gather needs several issuers;
-//   warp 3     MMA issuer; warps 4..7 softmax + per-token epilogue.
+// Warp roles (384 threads, 1 CTA / SM, persistent over (group, token)):
+//   warps 0..5 TMA producers -- warp w < 3 loads K, warp 3 + w loads V of
+//              ring stage w (pairs p = w mod 3): a single issuing thread tops
+//              out near 36 GB/s of TMA traffic (tools/gather_bench.cu), so
+//              the gather needs several issuers;
+//   warp 6     MMA issuer; warps 8..11 softmax + per-token epilogue.
 // Roofline: bound by the L2->SMEM gather of 2 x 63 x 16 KB per token
 // (K and V of the selected blocks); FLOP = 4 * 16 * 64 * d per block.
 #include <string.h>
@@ -34,8 +35,11 @@ namespace swattn {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kMmaWarp = 3;  // warps [0, kStages) produce, then MMA, then 4 softmax warps
+constexpr int kThreads = 384;
+// warps 0..2: K producers (stage w), 3..5: V producers (stage w-3), 6: MMA,
+// 7: idle, 8..11: softmax (TMEM lane quadrant = warp & 3)
+constexpr int kMmaWarp = 6;
+constexpr int kSoftmaxWarp0 = 8;
 constexpr int kStages = 3;
 constexpr int kBlk = 64;
 constexpr uint32_t kPairBytes = 2 * kBlk * kD * 2;  // 32 KB (K or V of two blocks)
@@ -116,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
   tc::tc_fence_after();
   const uint32_t tmem = s.tmem_base;
 
-  if (warp < kStages) {
+  if (warp < 2 * kStages) {
     // ------------------------------------------------------------ TMA producers
     // Whole warp walks the items; lane l holds block ids l and l+32 of the
     // current token, fetched one token ahead so no dependent global load sits
@@ -162,8 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
           const int x0 = 2 * pi, x1 = (2 * pi + 1 < cnt) ? 2 * pi + 1 : 2 * pi;  // odd tail: duplicate, masked
           const int b0 = __shfl_sync(0xffffffffu, x0 < 32 ? id0 : id1, x0 & 31);
           const int b1 = __shfl_sync(0xffffffffu, x1 < 32 ? id0 : id1, x1 & 31);
-          if (lane == 0 && (int)(pair % kStages) == warp) {
-            const int st = warp;
+          const bool is_v = warp >= kStages;
+          const int st = is_v ? warp - kStages : warp;
+          if (lane == 0 && (int)(pair % kStages) == st && !is_v) {
             const uint32_t ph = ((pair / kStages) & 1) ^ 1;
             tc::mbar_wait(&s.k_empty[st], ph);
             tc::mbar_arrive_expect_tx(&s.k_full[st], kPairBytes);
@@ -172,6 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
               tc::tma_load_2d(&p.k_map, &s.k_full[st], dst, g * kD + h * 64, b0 * kBlk);
               tc::tma_load_2d(&p.k_map, &s.k_full[st], dst + kBlk * 128, g * kD + h * 64, b1 * kBlk);
             }
+          }
+          if (lane == 0 && (int)(pair % kStages) == st && is_v) {
+            const uint32_t ph = ((pair / kStages) & 1) ^ 1;
             tc::mbar_wait(&s.v_empty[st], ph);
             tc::mbar_arrive_expect_tx(&s.v_full[st], kPairBytes);
             for (int h = 0; h < 2; ++h) {
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
       ++tau;
     }
     if (pend) issue_pv();
-  } else {
+  } else if (warp >= kSoftmaxWarp0) {
     // ------------------------------------------------------------ softmax / epilogue
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // key lane (S^T) / d lane (O^T)

@@ -48,9 +48,9 @@ __device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, i
   __syncwarp();
 
   // k-th largest key T: rounds of 8-bit radix select (warp-private 256-bin
-  // histogram, descending scan across lanes).  The bits every key shares
-  // (scores live in a narrow positive range) are skipped, and lanes that hit
-  // the same bin aggregate into one shared-memory atomic.
+  // histogram, descending scan across lanes).  The leading bits every key
+  // shares (scores live in a narrow positive range) are skipped, so the
+  // first histogram already spreads over many bins (low atomic contention).
   uint32_t kmin = 0xffffffffu, kmax = 0;
   for (int t = lane; t < ncand; t += 32) {
     kmin = min(kmin, ks[t]);
@@ -68,18 +68,10 @@ __device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, i
 #pragma unroll
     for (int e = 0; e < 8; ++e) hist[lane * 8 + e] = 0;
     __syncwarp();
-    for (int base = 0; base < ncand; base += 32) {
-      const int t = base + lane;
-      const uint32_t v = t < ncand ? ks[t] : 0u;
-      const bool ok = t < ncand && (v & pmask) == prefix;
-      const unsigned act = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const uint32_t bin = (v >> sh) & 255u;
-        const unsigned same = __match_any_sync(act, bin);
-        if ((__ffs(same) - 1) == lane) atomicAdd(&hist[bin], __popc(same));
-      }
+    for (int t = lane; t < ncand; t += 32) {
+      const uint32_t v = ks[t];
+      if ((v & pmask) == prefix) atomicAdd(&hist[(v >> sh) & 255u], 1);
     }
-    __syncwarp();
     __syncwarp();
     int cnt[8], tot = 0;  // lane owns bins 255-8*lane .. 248-8*lane (descending)
 #pragma unroll

@@ -1,4 +1,6 @@
 set -x
 export PYTHONUNBUFFERED=1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_pb -s 1 -c 1 -o gpurun_out/prof_pb2 python tools/one_attend.py 131072 > gpurun_out/ncu_pb2.log 2>&1; tail -2 gpurun_out/ncu_pb2.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:scores_tc -s 1 -c 1 -o gpurun_out/prof_sc2 python tools/one_attend.py 131072 > gpurun_out/ncu_sc2.log 2>&1; tail -2 gpurun_out/ncu_sc2.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -k "sparse or attend or full_size or decode or selection" 2>&1 | grep -E "passed|failed|Error|assert|FAIL" | head -20
+K='regex:compress|scores|topk|rerank|fa_tile|sparse_pb|attention_list'
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv --log-file gpurun_out/launches_128k.csv python tools/one_attend.py 131072 > /dev/null 2>&1
+grep -v "^==" gpurun_out/launches_128k.csv | awk -F'","' '{print $5, $NF}' | sed 's/"//g' | tail -8
