@@ -17,12 +17,18 @@
 // sparse_forward (sparse.py:70-91).  A token whose logits exceed m_A by more
 // than 2^64 is listed for the CUDA-core exact path (never on sane inputs).
 //
-// Warp roles (384 threads, 1 CTA / SM, persistent over (group, token)):
-//   warps 0..5 TMA producers -- warp w < 3 loads K, warp 3 + w loads V of
-//              ring stage w (pairs p = w mod 3): a single issuing thread tops
-//              out near 36 GB/s of TMA traffic (tools/gather_bench.cu), so
-//              the gather needs several issuers;
-//   warp 6     MMA issuer; warps 8..11 softmax + per-token epilogue.
+// Pipeline: the MMA issuer runs the S MMAs kLag pairs ahead of the PV MMAs,
+// so the softmax warps always have S tiles queued and the chain
+// S -> softmax -> PV never serialises the tensor pipe; K and V travel in
+// separate TMA rings (K is released right after S, V is held until its PV,
+// hence the deeper V ring).  Fixed-offset softmax makes the O accumulation
+// order-free, which is what allows the lag across token boundaries.
+//
+// Warp roles (320 threads, 1 CTA / SM, persistent over (group, token)):
+//   warps 0-1 K producers (ring stage q % 2), warps 2-3 V producers (stage
+//   parity), warps 4-7 softmax + per-token epilogue (TMEM lane quadrant =
+//   warp & 3), warp 8 MMA issuer.  Several issuing threads: one thread's TMA
+//   issue rate caps near 36 GB/s (tools/gather_bench.cu).
 // Roofline: bound by the L2->SMEM gather of 2 x 63 x 16 KB per token
 // (K and V of the selected blocks); FLOP = 4 * 16 * 64 * d per block.
 #include <string.h>
@@ -35,17 +41,20 @@ namespace swattn {
 
 namespace {
 
-constexpr int kThreads = 384;
-// warps 0..2: K producers (stage w), 3..5: V producers (stage w-3), 6: MMA,
-// 7: idle, 8..11: softmax (TMEM lane quadrant = warp & 3)
-constexpr int kMmaWarp = 6;
-constexpr int kSoftmaxWarp0 = 8;
-constexpr int kStages = 3;
+constexpr int kThreads = 288;
+constexpr int kSoftmaxWarp0 = 4;
+constexpr int kMmaWarp = 8;
+constexpr int kKStages = 2;
+constexpr int kVStages = 4;
+constexpr int kLag = 2;                 // S issued kLag pairs ahead of PV
+constexpr int kSBufs = kLag + 2;        // S tiles in TMEM
+constexpr int kPBufs = kLag + 2;        // P tiles in smem
 constexpr int kBlk = 64;
 constexpr uint32_t kPairBytes = 2 * kBlk * kD * 2;  // 32 KB (K or V of two blocks)
 constexpr uint32_t kQTokBytes = kG * kD * 2;          // 4 KB
 constexpr uint32_t kPBytes = kG * 128 * 2;            // 4 KB
-constexpr uint32_t kTmemCols = 64;                    // S0 S1 O0 O1 (16 each)
+constexpr uint32_t kTmemCols = 128;                   // S x4 | O x2 (16 cols each)
+constexpr uint32_t kTmemO = kSBufs * kG;
 constexpr float kOverflowExcess = 64.f;
 
 struct PbParams {
@@ -65,13 +74,13 @@ struct PbParams {
 };
 
 struct __align__(1024) PbSmem {
-  uint8_t k[kStages][kPairBytes];
-  uint8_t v[kStages][kPairBytes];
+  uint8_t k[kKStages][kPairBytes];
+  uint8_t v[kVStages][kPairBytes];
+  uint8_t p[kPBufs][kPBytes];
   uint8_t q[2][kQTokBytes];
-  uint8_t p[2][kPBytes];
-  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+  uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
   uint64_t q_full[2], q_empty[2];
-  uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2];
+  uint64_t s_full[kSBufs], s_empty[kSBufs], p_full[kPBufs], p_empty[kPBufs];
   uint64_t o_full[2], o_empty[2];
   float lred[4][kG];
   uint32_t tmem_base;
@@ -90,25 +99,34 @@ __device__ __forceinline__ int cnt_of(const PbParams &p, int64_t it) {
   return p.topk_cnt[(int64_t)g * p.n + t];
 }
 
+// ring position helpers: slot and phase parity of the q-th use
+__device__ __forceinline__ uint32_t phase(int64_t q, int ring) { return (uint32_t)((q / ring) & 1); }
+
 __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_constant__ PbParams p) {
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on smem_raw so accesses stay in the shared space
   PbSmem &s = *reinterpret_cast<PbSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
       tc::mbar_init(&s.k_full[i], 1);
       tc::mbar_init(&s.k_empty[i], 1);
+    }
+    for (int i = 0; i < kVStages; ++i) {
       tc::mbar_init(&s.v_full[i], 1);
       tc::mbar_init(&s.v_empty[i], 1);
+    }
+    for (int i = 0; i < kSBufs; ++i) {
+      tc::mbar_init(&s.s_full[i], 1);
+      tc::mbar_init(&s.s_empty[i], 128);
+    }
+    for (int i = 0; i < kPBufs; ++i) {
+      tc::mbar_init(&s.p_full[i], 128);
+      tc::mbar_init(&s.p_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s.q_full[i], 1);
       tc::mbar_init(&s.q_empty[i], 1);
-      tc::mbar_init(&s.s_full[i], 1);
-      tc::mbar_init(&s.s_empty[i], 128);
-      tc::mbar_init(&s.p_full[i], 128);
-      tc::mbar_init(&s.p_empty[i], 1);
       tc::mbar_init(&s.o_full[i], 1);
       tc::mbar_init(&s.o_empty[i], 128);
     }
@@ -120,17 +138,18 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
   tc::tc_fence_after();
   const uint32_t tmem = s.tmem_base;
 
-  if (warp < 2 * kStages) {
+  if (warp < kSoftmaxWarp0) {
     // ------------------------------------------------------------ TMA producers
-    // Whole warp walks the items; lane l holds block ids l and l+32 of the
-    // current token, fetched one token ahead so no dependent global load sits
-    // between two TMA issues (an L2 round trip per pair halves the gather rate).
+    // warps 0/1: K of pairs with q % 2 == warp; warps 2/3: V of pairs whose V
+    // stage (q % 4) has parity warp-2.  Each warp walks all items; lane l holds
+    // block ids l and l+32 of the current token, fetched one token ahead.
+    const bool is_v = warp >= 2;
+    const int role = warp & 1;
     if (lane == 0) {
       tc::tma_prefetch(&p.q_map);
-      tc::tma_prefetch(&p.k_map);
-      tc::tma_prefetch(&p.v_map);
+      tc::tma_prefetch(is_v ? &p.v_map : &p.k_map);
     }
-    int64_t pair = 0;
+    int64_t q = 0;
     int tau = 0;
     auto fetch = [&](int64_t item, int &cnt, int &id0, int &id1) {
       int g;
@@ -153,24 +172,22 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
         int g;
         int64_t t;
         item_of(p, it, g, t);
-        const int qs = tau & 1;
         if (lane == 0 && warp == 0) {
-          tc::mbar_wait(&s.q_empty[qs], ((tau >> 1) & 1) ^ 1);
+          const int qs = tau & 1;
+          tc::mbar_wait(&s.q_empty[qs], phase(tau, 2) ^ 1);
           tc::mbar_arrive_expect_tx(&s.q_full[qs], kQTokBytes);
           for (int h = 0; h < 2; ++h)
             tc::tma_load_3d(&p.q_map, &s.q_full[qs], s.q[qs] + h * (kQTokBytes / 2), h * 64,
                             g * kG, (int)t);
         }
         const int npairs = (cnt + 1) >> 1;
-        for (int pi = 0; pi < npairs; ++pi, ++pair) {
+        for (int pi = 0; pi < npairs; ++pi, ++q) {
           const int x0 = 2 * pi, x1 = (2 * pi + 1 < cnt) ? 2 * pi + 1 : 2 * pi;  // odd tail: duplicate, masked
           const int b0 = __shfl_sync(0xffffffffu, x0 < 32 ? id0 : id1, x0 & 31);
           const int b1 = __shfl_sync(0xffffffffu, x1 < 32 ? id0 : id1, x1 & 31);
-          const bool is_v = warp >= kStages;
-          const int st = is_v ? warp - kStages : warp;
-          if (lane == 0 && (int)(pair % kStages) == st && !is_v) {
-            const uint32_t ph = ((pair / kStages) & 1) ^ 1;
-            tc::mbar_wait(&s.k_empty[st], ph);
+          if (lane == 0 && !is_v && (int)(q % kKStages) == role) {
+            const int st = role;
+            tc::mbar_wait(&s.k_empty[st], phase(q, kKStages) ^ 1);
             tc::mbar_arrive_expect_tx(&s.k_full[st], kPairBytes);
             for (int h = 0; h < 2; ++h) {
               uint8_t *dst = s.k[st] + h * (kPairBytes / 2);
@@ -178,9 +195,9 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
               tc::tma_load_2d(&p.k_map, &s.k_full[st], dst + kBlk * 128, g * kD + h * 64, b1 * kBlk);
             }
           }
-          if (lane == 0 && (int)(pair % kStages) == st && is_v) {
-            const uint32_t ph = ((pair / kStages) & 1) ^ 1;
-            tc::mbar_wait(&s.v_empty[st], ph);
+          if (lane == 0 && is_v && (int)(q % kVStages) % 2 == role) {
+            const int st = (int)(q % kVStages);
+            tc::mbar_wait(&s.v_empty[st], phase(q, kVStages) ^ 1);
             tc::mbar_arrive_expect_tx(&s.v_full[st], kPairBytes);
             for (int h = 0; h < 2; ++h) {
               uint8_t *dst = s.v[st] + h * (kPairBytes / 2);
@@ -201,55 +218,53 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id_s = tc::idesc_bf16(128, kG, false, false);
     const uint32_t id_o = tc::idesc_bf16(128, kG, true, false);
-    int64_t pair = 0;      // global pair counter (S issued)
-    int tau = 0;
-    // deferred PV of the previous pair
-    bool pend = false;
-    int64_t pend_pair = 0;
-    bool pend_first = false, pend_last = false;
-    int pend_tau = 0;
+    // deferred PV queue (kLag entries): pair index, token, first/last flags
+    int64_t pq[kLag + 1];
+    int ptau[kLag + 1];
+    bool pfirst[kLag + 1], plast[kLag + 1];
+    int head = 0, npend = 0;
     auto issue_pv = [&]() {
-      const int st = (int)(pend_pair % kStages);
-      const int pb = (int)(pend_pair & 1);
-      tc::mbar_wait(&s.p_full[pb], (pend_pair >> 1) & 1);
-      tc::mbar_wait(&s.v_full[st], (pend_pair / kStages) & 1);
-      if (pend_first) tc::mbar_wait(&s.o_empty[pend_tau & 1], ((pend_tau >> 1) & 1) ^ 1);
+      const int64_t qq = pq[head];
+      const int tt = ptau[head];
+      const int vs = (int)(qq % kVStages), pb = (int)(qq % kPBufs);
+      tc::mbar_wait(&s.p_full[pb], phase(qq, kPBufs));
+      tc::mbar_wait(&s.v_full[vs], phase(qq, kVStages));
+      if (pfirst[head]) tc::mbar_wait(&s.o_empty[tt & 1], phase(tt, 2) ^ 1);
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const uint32_t v_addr = tc::smem_u32(s.v[st]);
+        const uint32_t v_addr = tc::smem_u32(s.v[vs]);
         const uint32_t p_addr = tc::smem_u32(s.p[pb]);
-        const uint32_t d_o = tmem + 32 + (pend_tau & 1) * kG;
+        const uint32_t d_o = tmem + kTmemO + (tt & 1) * kG;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           tc::mma_ss(d_o, tc::desc_mnmajor(v_addr + kk * 16 * 128, kPairBytes / 2),
                      tc::desc_kmajor(p_addr + (kk >> 2) * (kPBytes / 2) + (kk & 3) * 32), id_o,
-                     (!pend_first || kk > 0) ? 1u : 0u);
-        tc::mma_commit(&s.v_empty[st]);
+                     (!pfirst[head] || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&s.v_empty[vs]);
         tc::mma_commit(&s.p_empty[pb]);
-        if (pend_last) tc::mma_commit(&s.o_full[pend_tau & 1]);
+        if (plast[head]) tc::mma_commit(&s.o_full[tt & 1]);
       }
       __syncwarp();
-      pend = false;
+      head = (head + 1) % (kLag + 1);
+      --npend;
     };
+    int64_t q = 0;
+    int tau = 0;
     int cnt_next = blockIdx.x < p.n_items ? cnt_of(p, blockIdx.x) : 0;
     for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-      int g;
-      int64_t t;
-      item_of(p, it, g, t);
       const int cnt = cnt_next;  // fetched one item ahead
       cnt_next = it + gridDim.x < p.n_items ? cnt_of(p, it + gridDim.x) : 0;
       if (cnt == 0) continue;
       const int npairs = (cnt + 1) >> 1;
       const int qs = tau & 1;
-      tc::mbar_wait(&s.q_full[qs], (tau >> 1) & 1);
-      for (int pi = 0; pi < npairs; ++pi, ++pair) {
-        const int st = (int)(pair % kStages);
-        const int sb = (int)(pair & 1);
-        tc::mbar_wait(&s.k_full[st], (pair / kStages) & 1);
-        tc::mbar_wait(&s.s_empty[sb], ((pair >> 1) & 1) ^ 1);
+      tc::mbar_wait(&s.q_full[qs], phase(tau, 2));
+      for (int pi = 0; pi < npairs; ++pi, ++q) {
+        const int ks = (int)(q % kKStages), sb = (int)(q % kSBufs);
+        tc::mbar_wait(&s.k_full[ks], phase(q, kKStages));
+        tc::mbar_wait(&s.s_empty[sb], phase(q, kSBufs) ^ 1);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          const uint32_t k_addr = tc::smem_u32(s.k[st]);
+          const uint32_t k_addr = tc::smem_u32(s.k[ks]);
           const uint32_t q_addr = tc::smem_u32(s.q[qs]);
 #pragma unroll
           for (int kk = 0; kk < kD / 16; ++kk) {
@@ -258,26 +273,27 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
                        tc::desc_kmajor(q_addr + h * (kQTokBytes / 2) + j * 32), id_s, kk > 0);
           }
           tc::mma_commit(&s.s_full[sb]);
-          tc::mma_commit(&s.k_empty[st]);
+          tc::mma_commit(&s.k_empty[ks]);
           if (pi == npairs - 1) tc::mma_commit(&s.q_empty[qs]);
         }
         __syncwarp();
-        if (pend) issue_pv();
-        pend = true;
-        pend_pair = pair;
-        pend_first = pi == 0;
-        pend_last = pi == npairs - 1;
-        pend_tau = tau;
+        const int tail = (head + npend) % (kLag + 1);
+        pq[tail] = q;
+        ptau[tail] = tau;
+        pfirst[tail] = pi == 0;
+        plast[tail] = pi == npairs - 1;
+        ++npend;
+        if (npend > kLag) issue_pv();
       }
       ++tau;
     }
-    if (pend) issue_pv();
-  } else if (warp >= kSoftmaxWarp0) {
+    while (npend > 0) issue_pv();
+  } else {
     // ------------------------------------------------------------ softmax / epilogue
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // key lane (S^T) / d lane (O^T)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    int64_t pair = 0;
+    int64_t q = 0;
     int tau = 0;
     int cnt_next = blockIdx.x < p.n_items ? cnt_of(p, blockIdx.x) : 0;
     for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x) {
@@ -297,9 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
         lp[h] = 0.f;
       }
       float excess = -INFINITY;
-      for (int pi = 0; pi < npairs; ++pi, ++pair) {
-        const int sb = (int)(pair & 1);
-        tc::mbar_wait(&s.s_full[sb], (pair >> 1) & 1);
+      for (int pi = 0; pi < npairs; ++pi, ++q) {
+        const int sb = (int)(q % kSBufs), pb = (int)(q % kPBufs);
+        tc::mbar_wait(&s.s_full[sb], phase(q, kSBufs));
         tc::tc_fence_after();
         uint32_t sv[kG];
         tc::tmem_ld16(tmem + lane_off + sb * kG, sv);
@@ -307,25 +323,30 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
         tc::tc_fence_before();
         tc::mbar_arrive(&s.s_empty[sb]);
         const bool valid = (2 * pi + (r >> 6)) < cnt;
-        float pr[kG];
+        uint32_t pk[kG / 2];
 #pragma unroll
-        for (int h = 0; h < kG; ++h) {
-          const float x = __uint_as_float(sv[h]) * p.scale_log2 - mA[h];
-          excess = valid ? fmaxf(excess, x) : excess;
-          pr[h] = valid ? fast_exp2(x) : 0.f;
-          lp[h] += pr[h];
+        for (int h = 0; h < kG; h += 2) {
+          const float x0 = __uint_as_float(sv[h]) * p.scale_log2 - mA[h];
+          const float x1 = __uint_as_float(sv[h + 1]) * p.scale_log2 - mA[h + 1];
+          excess = valid ? fmaxf(excess, fmaxf(x0, x1)) : excess;
+          const float p0 = valid ? fast_exp2(x0) : 0.f;
+          const float p1 = valid ? fast_exp2(x1) : 0.f;
+          lp[h] += p0;
+          lp[h + 1] += p1;
+          pk[h / 2] = tc::pack_bf16(p0, p1);
         }
         // P^T tile (K-major: row = head, 128 keys in two 64-key halves)
-        tc::mbar_wait(&s.p_empty[sb], ((pair >> 1) & 1) ^ 1);
-        uint8_t *pt = s.p[sb] + (r >> 6) * (kPBytes / 2);
+        tc::mbar_wait(&s.p_empty[pb], phase(q, kPBufs) ^ 1);
+        uint8_t *pt = s.p[pb] + (r >> 6) * (kPBytes / 2);
         const int c = r & 63;
 #pragma unroll
         for (int h = 0; h < kG; ++h) {
           const uint32_t off = h * 128 + ((((c * 2) >> 4) ^ (h & 7)) << 4) + ((c * 2) & 15);
-          *reinterpret_cast<__nv_bfloat16 *>(pt + off) = __float2bfloat16_rn(pr[h]);
+          const uint32_t w = pk[h / 2];
+          *reinterpret_cast<uint16_t *>(pt + off) = (h & 1) ? (uint16_t)(w >> 16) : (uint16_t)w;
         }
         tc::fence_proxy_async();
-        tc::mbar_arrive(&s.p_full[sb]);
+        tc::mbar_arrive(&s.p_full[pb]);
       }
       // ---- per-token epilogue
 #pragma unroll
@@ -334,20 +355,16 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         lp[h] = v;
       }
-      excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, 16));
-      excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, 8));
-      excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, 4));
-      excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, 2));
-      excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, 1));
+      for (int o = 16; o; o >>= 1) excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, o));
       if (lane == 0) {
 #pragma unroll
         for (int h = 0; h < kG; ++h) s.lred[quad][h] = lp[h];
       }
       const int ob = tau & 1;
-      tc::mbar_wait(&s.o_full[ob], (tau >> 1) & 1);
+      tc::mbar_wait(&s.o_full[ob], phase(tau, 2));
       tc::tc_fence_after();
       uint32_t ov[kG];
-      tc::tmem_ld16(tmem + lane_off + 32 + ob * kG, ov);
+      tc::tmem_ld16(tmem + lane_off + kTmemO + ob * kG, ov);
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&s.o_empty[ob]);
@@ -357,8 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
 #pragma unroll
       for (int h = 0; h < kG; ++h)
         lB[h] = s.lred[0][h] + s.lred[1][h] + s.lred[2][h] + s.lred[3][h];
-      float exw = excess;
-      if (exw > kOverflowExcess && lane == 0) {
+      if (excess > kOverflowExcess && r == 0) {
         const int slot = atomicAdd(p.slow_count, 1);
         p.slow_list[slot] = (int32_t)row;
       }
