@@ -63,10 +63,20 @@ struct __align__(1024) ScSmem {
   uint8_t k[kStages][kKBytes];
   uint64_t q_full, full[kStages], empty[kStages], tfull[2], tempty[2];
   __align__(16) float2 stat[kRows];  // (m, 1/l) per (token, head) row, log2 domain
-  uint32_t edge[4][kTok];      // warp-boundary column values for the max-pool
-  uint32_t flw[4][kTok];       // per-warp flag bits (16 per warp) per token
+  float sc[kTok][kCols + 4];   // tile column scores for the max-pool
   uint32_t tmem_base;
 };
+
+// bit q of x -> bit 2q of the result (Morton spread)
+__device__ __forceinline__ unsigned long long spread_bits(uint32_t x) {
+  unsigned long long v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
 
 __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_constant__ ScParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -201,13 +211,12 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
     asm volatile("bar.sync 1, 128;" ::: "memory");
 
     // ---------------- pass 2: thread = C1 column of the tile
-    int v1k[kTok];
-#pragma unroll
-    for (int k = 0; k < kTok; ++k) v1k[k] = (int)vis_count(i0 + k, p.l_C1, p.s_C1);
+    // No causal / edge masking is needed here: every column of a candidate
+    // block's window (cols <= 4*hi) is visible to all 8 rows (vis1 >= 4b - 1)
+    // and < m1; values of other columns are never written.
     for (int t = 0; t < n_t2; ++t) {
       const int u = n_c1 + t;
       const int tb = u & 1;
-      const int col = t * kTileStride + r;
       tc::mbar_wait(&s.tfull[tb], (u >> 1) & 1);
       tc::tc_fence_after();
       float sc[kTok];
@@ -236,57 +245,43 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
             a3 = fmaf(fast_exp2(fmaf(__uint_as_float(u3), p.scale_log2, -st23.z)), st23.w, a3);
           }
           const float acc = (a0 + a1) + (a2 + a3);
-          sc[kb + k] = (col >= p.m1) ? -INFINITY : ((col < v1k[kb + k]) ? acc : 0.f);
+          sc[kb + k] = acc;
         }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&s.tempty[tb]);
-      // warp-boundary column (lane 0 of the next warp) for blocks 7, 15, 23
-      if (lane == 0) {
+      // stage the tile's column scores [token][column]; the 5/4 max-pool then
+      // runs one block per lane (warp w pools tokens w and w+4), so the 31
+      // block scores of a token are written coalesced and the tie flags come
+      // straight out of two ballots
 #pragma unroll
-        for (int k = 0; k < kTok; ++k) s.edge[quad][k] = __float_as_uint(sc[k]);
-      }
+      for (int k = 0; k < kTok; ++k) s.sc[k][r] = sc[k];
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int qb = r >> 2;                  // block within the tile
-      const bool head_lane = (r & 3) == 0 && qb < kTileBlocks;
-      const int j = t * kTileBlocks + qb;     // global block index
-      const bool write = head_lane && j >= p.N_init && j < hi;
+      const int qb = lane;
+      const int j = t * kTileBlocks + qb;
+      const bool blk_ok = qb < kTileBlocks && j >= p.N_init && j < hi;
 #pragma unroll
-      for (int k = 0; k < kTok; ++k) {
-        const float v0 = sc[k];
-        const float v1 = __shfl_down_sync(0xffffffffu, v0, 1);
-        const float v2 = __shfl_down_sync(0xffffffffu, v0, 2);
-        const float v3 = __shfl_down_sync(0xffffffffu, v0, 3);
-        float v4 = __shfl_down_sync(0xffffffffu, v0, 4);
-        if (lane == 28) v4 = __uint_as_float(s.edge[(quad + 1) & 3][k]);
-        const float mx = fmaxf(fmaxf(fmaxf(v0, v1), fmaxf(v2, v3)), v4);
+      for (int kk = 0; kk < 2; ++kk) {
+        const int k = quad + 4 * kk;
         const int64_t tok = i0 + k;
-        const bool ok = write && tok < p.n;
+        const bool ok = blk_ok && tok < p.n;
+        float v[kPoolL];
+#pragma unroll
+        for (int e = 0; e < kPoolL; ++e) v[e] = s.sc[k][min(qb * kPoolS + e, kCols - 1)];
+        const float mx = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), v[4]);
         if (ok) p.s_cmp[((int64_t)g * p.n + tok) * p.ld + j] = mx;
         if (p.flags != nullptr) {
           // argmax-at-shared-column bits (L: window col 0, R: col 4) with margin
           const float f = 1.f + 4.f * kScoreRelErr;
-          const bool L = ok && v1 * f < v0 && v2 * f < v0 && v3 * f < v0 && v4 * f < v0;
-          const bool R = ok && v0 * f < v4 && v1 * f < v4 && v2 * f < v4 && v3 * f < v4;
+          const bool L = ok && v[1] * f < v[0] && v[2] * f < v[0] && v[3] * f < v[0] && v[4] * f < v[0];
+          const bool R = ok && v[0] * f < v[4] && v[1] * f < v[4] && v[2] * f < v[4] && v[3] * f < v[4];
           const unsigned lm = __ballot_sync(0xffffffffu, L);
           const unsigned rm = __ballot_sync(0xffffffffu, R);
-          if (lane == 0) {
-            uint32_t w = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              w |= (((lm >> (4 * e)) & 1u) << (2 * e)) | (((rm >> (4 * e)) & 1u) << (2 * e + 1));
-            s.flw[quad][k] = w;
-          }
+          if (lane == 0 && tok < p.n)
+            p.flags[((int64_t)g * p.n + tok) * p.ld_f + t] = spread_bits(lm) | (spread_bits(rm) << 1);
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (p.flags != nullptr && r < kTok && i0 + r < p.n) {
-        const unsigned long long w = (unsigned long long)s.flw[0][r] |
-                                     ((unsigned long long)s.flw[1][r] << 16) |
-                                     ((unsigned long long)s.flw[2][r] << 32) |
-                                     ((unsigned long long)s.flw[3][r] << 48);
-        p.flags[((int64_t)g * p.n + i0 + r) * p.ld_f + t] = w;
-      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // s.sc reuse by the next tile
     }
   }
   tc::tc_fence_before();
