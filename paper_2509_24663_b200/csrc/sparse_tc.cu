@@ -53,7 +53,7 @@ constexpr int kBlk = 64;
 constexpr uint32_t kPairBytes = 2 * kBlk * kD * 2;  // 32 KB (K or V of two blocks)
 constexpr uint32_t kQTokBytes = kG * kD * 2;          // 4 KB
 constexpr uint32_t kPBytes = kG * 128 * 2;            // 4 KB
-constexpr uint32_t kTmemCols = 128;                   // S x4 | O x2 (16 cols each)
+constexpr uint32_t kTmemCols = 128;                   // S x4 | O 2 tokens x 2 accumulators
 constexpr uint32_t kTmemO = kSBufs * kG;
 constexpr float kOverflowExcess = 64.f;
 
@@ -216,37 +216,84 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    // An N = 16 MMA chain accumulating into one TMEM tile is latency-bound
+    // (~130 cycles per dependent MMA while the tensor pipe is 95 % idle), so
+    // pairs are issued two at a time with their k-steps interleaved: S of
+    // pairs (q, q+1) and PV of the previous two pairs form four independent
+    // accumulation chains.  PV of a token alternates between two O
+    // accumulators (pair parity), summed in the epilogue.
     const uint32_t id_s = tc::idesc_bf16(128, kG, false, false);
     const uint32_t id_o = tc::idesc_bf16(128, kG, true, false);
-    // deferred PV queue (kLag entries): pair index, token, first/last flags
-    int64_t pq[kLag + 1];
-    int ptau[kLag + 1];
-    bool pfirst[kLag + 1], plast[kLag + 1];
-    int head = 0, npend = 0;
-    auto issue_pv = [&]() {
-      const int64_t qq = pq[head];
-      const int tt = ptau[head];
-      const int vs = (int)(qq % kVStages), pb = (int)(qq % kPBufs);
-      tc::mbar_wait(&s.p_full[pb], phase(qq, kPBufs));
-      tc::mbar_wait(&s.v_full[vs], phase(qq, kVStages));
-      if (pfirst[head]) tc::mbar_wait(&s.o_empty[tt & 1], phase(tt, 2) ^ 1);
+    struct PairInfo {
+      int64_t q;
+      int tau, pi, npairs;
+    };
+    PairInfo cur[2], pv[2];
+    int ncur = 0, npv = 0;
+    auto issue_pv_group = [&]() {
+      for (int e = 0; e < npv; ++e) {
+        const int64_t qq = pv[e].q;
+        tc::mbar_wait(&s.p_full[(int)(qq % kPBufs)], phase(qq, kPBufs));
+        tc::mbar_wait(&s.v_full[(int)(qq % kVStages)], phase(qq, kVStages));
+        if (pv[e].pi == 0) tc::mbar_wait(&s.o_empty[pv[e].tau & 1], phase(pv[e].tau, 2) ^ 1);
+      }
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const uint32_t v_addr = tc::smem_u32(s.v[vs]);
-        const uint32_t p_addr = tc::smem_u32(s.p[pb]);
-        const uint32_t d_o = tmem + kTmemO + (tt & 1) * kG;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_ss(d_o, tc::desc_mnmajor(v_addr + kk * 16 * 128, kPairBytes / 2),
-                     tc::desc_kmajor(p_addr + (kk >> 2) * (kPBytes / 2) + (kk & 3) * 32), id_o,
-                     (!pfirst[head] || kk > 0) ? 1u : 0u);
-        tc::mma_commit(&s.v_empty[vs]);
-        tc::mma_commit(&s.p_empty[pb]);
-        if (plast[head]) tc::mma_commit(&s.o_full[tt & 1]);
+        for (int kk = 0; kk < 8; ++kk) {
+          for (int e = 0; e < npv; ++e) {
+            const int64_t qq = pv[e].q;
+            const uint32_t v_addr = tc::smem_u32(s.v[(int)(qq % kVStages)]);
+            const uint32_t p_addr = tc::smem_u32(s.p[(int)(qq % kPBufs)]);
+            const uint32_t d_o = tmem + kTmemO + ((pv[e].tau & 1) * 2 + (pv[e].pi & 1)) * kG;
+            tc::mma_ss(d_o, tc::desc_mnmajor(v_addr + kk * 16 * 128, kPairBytes / 2),
+                       tc::desc_kmajor(p_addr + (kk >> 2) * (kPBytes / 2) + (kk & 3) * 32), id_o,
+                       (pv[e].pi >= 2 || kk > 0) ? 1u : 0u);
+          }
+        }
+        for (int e = 0; e < npv; ++e) {
+          const int64_t qq = pv[e].q;
+          tc::mma_commit(&s.v_empty[(int)(qq % kVStages)]);
+          tc::mma_commit(&s.p_empty[(int)(qq % kPBufs)]);
+          if (pv[e].pi == pv[e].npairs - 1) tc::mma_commit(&s.o_full[pv[e].tau & 1]);
+        }
       }
       __syncwarp();
-      head = (head + 1) % (kLag + 1);
-      --npend;
+      npv = 0;
+    };
+    auto flush = [&]() {
+      for (int e = 0; e < ncur; ++e) {
+        const int64_t qq = cur[e].q;
+        if (cur[e].pi == 0) tc::mbar_wait(&s.q_full[cur[e].tau & 1], phase(cur[e].tau, 2));
+        tc::mbar_wait(&s.k_full[(int)(qq % kKStages)], phase(qq, kKStages));
+        tc::mbar_wait(&s.s_empty[(int)(qq % kSBufs)], phase(qq, kSBufs) ^ 1);
+      }
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const int h = kk >> 2, j = kk & 3;
+          for (int e = 0; e < ncur; ++e) {
+            const int64_t qq = cur[e].q;
+            const uint32_t k_addr = tc::smem_u32(s.k[(int)(qq % kKStages)]);
+            const uint32_t q_addr = tc::smem_u32(s.q[cur[e].tau & 1]);
+            tc::mma_ss(tmem + (int)(qq % kSBufs) * kG,
+                       tc::desc_kmajor(k_addr + h * (kPairBytes / 2) + j * 32),
+                       tc::desc_kmajor(q_addr + h * (kQTokBytes / 2) + j * 32), id_s, kk > 0);
+          }
+        }
+        for (int e = 0; e < ncur; ++e) {
+          const int64_t qq = cur[e].q;
+          tc::mma_commit(&s.s_full[(int)(qq % kSBufs)]);
+          tc::mma_commit(&s.k_empty[(int)(qq % kKStages)]);
+          if (cur[e].pi == cur[e].npairs - 1) tc::mma_commit(&s.q_empty[cur[e].tau & 1]);
+        }
+      }
+      __syncwarp();
+      if (npv) issue_pv_group();
+      for (int e = 0; e < ncur; ++e) pv[e] = cur[e];
+      npv = ncur;
+      ncur = 0;
     };
     int64_t q = 0;
     int tau = 0;
@@ -256,38 +303,14 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
       cnt_next = it + gridDim.x < p.n_items ? cnt_of(p, it + gridDim.x) : 0;
       if (cnt == 0) continue;
       const int npairs = (cnt + 1) >> 1;
-      const int qs = tau & 1;
-      tc::mbar_wait(&s.q_full[qs], phase(tau, 2));
       for (int pi = 0; pi < npairs; ++pi, ++q) {
-        const int ks = (int)(q % kKStages), sb = (int)(q % kSBufs);
-        tc::mbar_wait(&s.k_full[ks], phase(q, kKStages));
-        tc::mbar_wait(&s.s_empty[sb], phase(q, kSBufs) ^ 1);
-        tc::tc_fence_after();
-        if (tc::elect_one()) {
-          const uint32_t k_addr = tc::smem_u32(s.k[ks]);
-          const uint32_t q_addr = tc::smem_u32(s.q[qs]);
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const int h = kk >> 2, j = kk & 3;
-            tc::mma_ss(tmem + sb * kG, tc::desc_kmajor(k_addr + h * (kPairBytes / 2) + j * 32),
-                       tc::desc_kmajor(q_addr + h * (kQTokBytes / 2) + j * 32), id_s, kk > 0);
-          }
-          tc::mma_commit(&s.s_full[sb]);
-          tc::mma_commit(&s.k_empty[ks]);
-          if (pi == npairs - 1) tc::mma_commit(&s.q_empty[qs]);
-        }
-        __syncwarp();
-        const int tail = (head + npend) % (kLag + 1);
-        pq[tail] = q;
-        ptau[tail] = tau;
-        pfirst[tail] = pi == 0;
-        plast[tail] = pi == npairs - 1;
-        ++npend;
-        if (npend > kLag) issue_pv();
+        cur[ncur++] = PairInfo{q, tau, pi, npairs};
+        if (ncur == 2) flush();
       }
       ++tau;
     }
-    while (npend > 0) issue_pv();
+    if (ncur) flush();
+    if (npv) issue_pv_group();
   } else {
     // ------------------------------------------------------------ softmax / epilogue
     const int quad = warp & 3;
@@ -363,9 +386,15 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pb_kernel(const __grid_con
       const int ob = tau & 1;
       tc::mbar_wait(&s.o_full[ob], phase(tau, 2));
       tc::tc_fence_after();
-      uint32_t ov[kG];
-      tc::tmem_ld16(tmem + lane_off + kTmemO + ob * kG, ov);
+      uint32_t ov[kG], ov1[kG];
+      tc::tmem_ld16(tmem + lane_off + kTmemO + (ob * 2) * kG, ov);
+      tc::tmem_ld16(tmem + lane_off + kTmemO + (ob * 2 + 1) * kG, ov1);
       tc::tmem_ld_wait();
+      if (npairs >= 2) {
+#pragma unroll
+        for (int h = 0; h < kG; ++h)
+          ov[h] = __float_as_uint(__uint_as_float(ov[h]) + __uint_as_float(ov1[h]));
+      }
       tc::tc_fence_before();
       tc::mbar_arrive(&s.o_empty[ob]);
       // all 4 softmax warps: reduce the per-warp partial sums through smem
