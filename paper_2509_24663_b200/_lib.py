@@ -11,7 +11,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libswattn_b200.so")
+# SWATTN_B200_LIB: an alternative in-tree build of the same library (kernel A/B
+# experiments under tools/); never a different implementation.
+LIB_PATH = os.environ.get("SWATTN_B200_LIB") or os.path.join(_HERE, "libswattn_b200.so")
 
 SWATTN_OK = 0
 SWATTN_EINVAL = 1
