@@ -66,7 +66,6 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
   __shared__ int members[kMaxCluster];
   __shared__ double mscore[kMaxCluster];
   __shared__ int n_members, n_above;
-  __shared__ int out_s[kTopMax];
 
   const int total = min(*a.count, a.cap);
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -218,11 +217,20 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     }
     __syncthreads();
 
-    // ---- settle: slots = k - above; rank members by (score desc, index asc)
+    // ---- settle: slots = k - above; rank members by (score desc, index asc).
+    // The row's selection is then a bitmap over the candidates (above-cluster
+    // blocks + chosen members) in the now idle staging buffer, emitted in
+    // ascending order by a block-wide scan of per-thread word counts.
+    uint32_t *bits = reinterpret_cast<uint32_t *>(kc_s);
+    int *wsum = reinterpret_cast<int *>(kc_s) + (kChunk * kD * 2 - kThreads);  // tail of kc_s
+    const int nwords = (ncand + 31) >> 5;
+    for (int w = threadIdx.x; w < nwords; w += kThreads) bits[w] = 0u;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ncand; t += kThreads)
+      if (src[a.N_init + t] > vk + band) atomicOr(&bits[t >> 5], 1u << (t & 31));
     if (threadIdx.x == 0) {
       const int slots = k - n_above;
       // selection sort over the (small) cluster
-      int chosen = 0;
       for (int s = 0; s < slots && s < nm; ++s) {
         int best = -1;
         for (int mi = 0; mi < nm; ++mi) {
@@ -231,28 +239,38 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
               (mscore[mi] == mscore[best] && members[mi] < members[best]))
             best = mi;
         }
-        out_s[chosen++] = members[best];
-        members[best] = -1 - members[best];  // mark taken (keeps value recoverable)
+        const int t = members[best] - a.N_init;
+        atomicOr(&bits[t >> 5], 1u << (t & 31));
+        members[best] = -1 - members[best];  // mark taken
       }
-      // merge: above-cluster blocks + chosen, ascending
-      int w = 0;
-      int32_t *out = a.topk + (int64_t)row * a.k_top;
-      int ci = 0;
-      // sort chosen ascending (tiny)
-      for (int x = 1; x < chosen; ++x) {
-        int v = out_s[x], y = x - 1;
-        while (y >= 0 && out_s[y] > v) { out_s[y + 1] = out_s[y]; --y; }
-        out_s[y + 1] = v;
-      }
-      for (int t = 0; t < ncand; ++t) {
-        const int j = a.N_init + t;
-        const bool above = src[j] > vk + band;
-        while (ci < chosen && out_s[ci] < j) out[w++] = out_s[ci++];
-        if (above) out[w++] = j;
-      }
-      while (ci < chosen) out[w++] = out_s[ci++];
-      for (; w < a.k_top; ++w) out[w] = -1;
     }
+    __syncthreads();
+    // thread = contiguous run of words; exclusive scan of the run popcounts
+    const int per = (nwords + kThreads - 1) / kThreads;
+    const int w0 = threadIdx.x * per, w1 = min(w0 + per, nwords);
+    int mine = 0;
+    for (int w = w0; w < w1; ++w) mine += __popc(bits[w]);
+    int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int base = incl - mine;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    int total_sel = 0;
+    for (int w = 0; w < kThreads / 32; ++w) total_sel += wsum[w];
+    int32_t *out = a.topk + (int64_t)row * a.k_top;
+    for (int w = w0; w < w1; ++w) {
+      uint32_t x = bits[w];
+      while (x) {
+        const int bit = __ffs(x) - 1;
+        x &= x - 1;
+        out[base++] = a.N_init + (w << 5) + bit;
+      }
+    }
+    for (int t = total_sel + threadIdx.x; t < a.k_top; t += kThreads) out[t] = -1;
     __syncthreads();
   }
 }

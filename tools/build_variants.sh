@@ -18,6 +18,6 @@ for spec in "$@"; do
     done
   fi
   if [ -d $ROOT/tools/variants_src/$name ]; then cp $ROOT/tools/variants_src/$name/* $d/lib/csrc/; fi
-  make -s -C $d/lib/csrc -j8 > $d/build.log 2>&1 || { tail -20 $d/build.log; exit 1; }
+  make -s -C $d/lib/csrc -j8 EXTRA="$EXTRA" > $d/build.log 2>&1 || { tail -20 $d/build.log; exit 1; }
   echo "built $d/lib/libswattn_b200.so"
 done
