@@ -24,7 +24,8 @@
 //
 // Data movement: each warp streams its token's selected blocks as 16-key
 // stages (K and V, 4 KB each, one 4-D TMA box per tensor, 128-byte swizzle)
-// through its own 3-stage mbarrier ring; lane 0 is the warp's TMA issuer, so
+// through its own 2-stage mbarrier ring (8 warps x 2 stages measured best:
+// tools/probe_variants.sh sweep, 37.5 ms vs 41.5 ms for 3 stages at 128K); lane 0 is the warp's TMA issuer, so
 // a CTA has 8 independent issuers (a single issuing thread caps near
 // 36 GB/s, tools/gather_bench.cu).  The ring runs across token boundaries and
 // the next token's Q is fetched while the current one computes.
@@ -39,10 +40,20 @@ namespace swattn {
 
 namespace {
 
-constexpr int kWarps = 8;
+// geometry (overridable for tuning sweeps: tools/build_variants.sh EXTRA=-D...)
+#ifndef SWATTN_PW_WARPS
+#define SWATTN_PW_WARPS 8
+#endif
+#ifndef SWATTN_PW_STAGES
+#define SWATTN_PW_STAGES 2
+#endif
+#ifndef SWATTN_PW_STAGE_KEYS
+#define SWATTN_PW_STAGE_KEYS 16
+#endif
+constexpr int kWarps = SWATTN_PW_WARPS;
 constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 3;
-constexpr int kStageKeys = 16;
+constexpr int kStages = SWATTN_PW_STAGES;
+constexpr int kStageKeys = SWATTN_PW_STAGE_KEYS;
 constexpr int kBlk = 64;
 constexpr int kStagesPerBlock = kBlk / kStageKeys;       // 4
 constexpr uint32_t kTileBytes = kStageKeys * kD * 2;     // 4 KB (K or V of one stage)
@@ -50,8 +61,8 @@ constexpr uint32_t kQBytes = kG * kD * 2;                // 4 KB
 constexpr float kOverflowExcess = 64.f;
 
 struct PwParams {
-  CUtensorMap q_map;  // Q viewed [n][h_q][2][64]: box {64, 2, 16, 1}
-  CUtensorMap k_map;  // K viewed [n][h_kv][2][64]: box {64, 2, 1, 16}
+  CUtensorMap q_map;  // Q as (d lo/hi 64, head, half, token): box {64, 16, 2, 1}
+  CUtensorMap k_map;  // K as (d lo/hi 64, token, half, group): box {64, 16, 2, 1}
   CUtensorMap v_map;
   int64_t n;
   int h_q, h_kv, k_top;
@@ -82,10 +93,14 @@ __device__ __forceinline__ void item_of(const PwParams &p, int64_t it, int &g, i
   t = p.tok0 + it % per;
 }
 
-// byte offset of 16-byte chunk `c` (0..15) of 128-byte-swizzled line pair
-// `row` (a 256-byte row split into two 128-byte lines by the TMA box)
+// Tiles are stored [d half][row][64] (the tensor maps list the half after the
+// row dimension), so the 8 rows of an ldmatrix 8x8 matrix fall on 8
+// consecutive 128-byte lines and the 128-byte swizzle spreads them over all
+// banks.  Byte offset of 16-byte chunk `c` (0..15, i.e. d / 8) of `row` in a
+// tile of `rows` rows:
+template <int kRows>
 __device__ __forceinline__ uint32_t swz(int row, int c) {
-  const int line = row * 2 + (c >> 3);
+  const int line = (c >> 3) * kRows + row;
   return (uint32_t)(line * 128 + (((c & 7) ^ (line & 7)) << 4));
 }
 
@@ -172,15 +187,15 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
       const int st = (int)(issued % kStages);
       const int row0 = blk * kBlk + (prod.s % kStagesPerBlock) * kStageKeys;
       tc::mbar_arrive_expect_tx(&full[st], 2 * kTileBytes);
-      tc::tma_load_4d(&p.k_map, &full[st], ws.k[st], 0, 0, prod.g, row0);
-      tc::tma_load_4d(&p.v_map, &full[st], ws.v[st], 0, 0, prod.g, row0);
+      tc::tma_load_4d(&p.k_map, &full[st], ws.k[st], 0, row0, 0, prod.g);
+      tc::tma_load_4d(&p.v_map, &full[st], ws.v[st], 0, row0, 0, prod.g);
     }
     ++issued;
     prod.advance(p, lane);
   };
   if (lane == 0) {
     tc::mbar_arrive_expect_tx(qfull, kQBytes);
-    tc::tma_load_4d(&p.q_map, qfull, ws.q, 0, 0, prod.g * kG, (int)prod.t);
+    tc::tma_load_4d(&p.q_map, qfull, ws.q, 0, prod.g * kG, 0, (int)prod.t);
   }
   for (int i = 0; i < kStages && prod.valid(p); ++i) issue();
 
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     for (int ks = 0; ks < 8; ++ks) {
       // matrices: (heads 0-7, d lo), (heads 8-15, d lo), (heads 0-7, d hi), (heads 8-15, d hi)
       const int head = (lm & 1) * 8 + lr;
-      ldsm_x4(qaddr + swz(head, ks * 2 + (lm >> 1)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+      ldsm_x4(qaddr + swz<kG>(head, ks * 2 + (lm >> 1)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
     }
     // next token's Q streams in while this token computes
     {
@@ -216,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
       if (lane == 0 && nx.valid(p)) {
         tc::fence_proxy_async();
         tc::mbar_arrive_expect_tx(qfull, kQBytes);
-        tc::tma_load_4d(&p.q_map, qfull, ws.q, 0, 0, nx.g * kG, (int)nx.t);
+        tc::tma_load_4d(&p.q_map, qfull, ws.q, 0, nx.g * kG, 0, (int)nx.t);
       }
     }
     const float mA0 = p.m_a[ridx + h0], mA1 = p.m_a[ridx + h0 + 8];
@@ -230,6 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
       const int st = (int)(consumed % kStages);
       tc::mbar_wait(&full[st], (uint32_t)((consumed / kStages) & 1));
       const uint32_t kst = kbase + st * kTileBytes, vst = vbase + st * kTileBytes;
+#pragma unroll
+      for (int sub = 0; sub < kStageKeys / 16; ++sub) {
       // ---- S = Q K^T over 16 keys: n-tiles (keys 0-7, 8-15)
       float sc[2][4];
 #pragma unroll
@@ -238,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
       for (int ks = 0; ks < 8; ++ks) {
         // matrices: (keys 0-7, d lo), (keys 0-7, d hi), (keys 8-15, d lo), (keys 8-15, d hi)
         uint32_t b00, b01, b10, b11;
-        ldsm_x4(kst + swz((lm >> 1) * 8 + lr, ks * 2 + (lm & 1)), b00, b01, b10, b11);
+        ldsm_x4(kst + swz<kStageKeys>(sub * 16 + (lm >> 1) * 8 + lr, ks * 2 + (lm & 1)), b00, b01, b10, b11);
         mma16816(sc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b00, b01);
         mma16816(sc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b10, b11);
       }
@@ -264,9 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
         // matrices: (keys 0-7, d tile 2dp), (keys 8-15, d tile 2dp),
         //           (keys 0-7, d tile 2dp+1), (keys 8-15, d tile 2dp+1)
         uint32_t v00, v01, v10, v11;
-        ldsm_x4_t(vst + swz((lm & 1) * 8 + lr, dp * 2 + (lm >> 1)), v00, v01, v10, v11);
+        ldsm_x4_t(vst + swz<kStageKeys>(sub * 16 + (lm & 1) * 8 + lr, dp * 2 + (lm >> 1)), v00, v01, v10, v11);
         mma16816(o[2 * dp], pa0, pa1, pa2, pa3, v00, v01);
         mma16816(o[2 * dp + 1], pa0, pa1, pa2, pa3, v10, v11);
+      }
       }
       // ---- refill this slot with the stage kStages ahead (ring runs across tokens)
       __syncwarp();
@@ -321,18 +339,18 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
   PwParams p;
   memset(&p, 0, sizeof(p));
   {
-    const uint64_t dims[4] = {64, 2, (uint64_t)cfg->h_q, (uint64_t)n};
-    const uint64_t str[3] = {128, (uint64_t)kD * 2, (uint64_t)cfg->h_q * kD * 2};
-    const uint32_t box[4] = {64, 2, (uint32_t)kG, 1};
+    const uint64_t dims[4] = {64, (uint64_t)cfg->h_q, 2, (uint64_t)n};
+    const uint64_t str[3] = {(uint64_t)kD * 2, 128, (uint64_t)cfg->h_q * kD * 2};
+    const uint32_t box[4] = {64, (uint32_t)kG, 2, 1};
     if (!make_tmap_bf16(&p.q_map, Q, 4, dims, str, box)) {
       set_error("cuTensorMapEncodeTiled(Q) failed");
       return SWATTN_ECUDA;
     }
   }
   {
-    const uint64_t dims[4] = {64, 2, (uint64_t)cfg->h_kv, (uint64_t)n};
-    const uint64_t str[3] = {128, (uint64_t)kD * 2, (uint64_t)cfg->h_kv * kD * 2};
-    const uint32_t box[4] = {64, 2, 1, (uint32_t)kStageKeys};
+    const uint64_t dims[4] = {64, (uint64_t)n, 2, (uint64_t)cfg->h_kv};
+    const uint64_t str[3] = {(uint64_t)cfg->h_kv * kD * 2, 128, (uint64_t)kD * 2};
+    const uint32_t box[4] = {64, (uint32_t)kStageKeys, 2, 1};
     if (!make_tmap_bf16(&p.k_map, K, 4, dims, str, box) ||
         !make_tmap_bf16(&p.v_map, V, 4, dims, str, box)) {
       set_error("cuTensorMapEncodeTiled(K/V) failed");
