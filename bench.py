@@ -281,9 +281,16 @@ def run_ours(args):
                          "peak_source": f"{peaks['source']} "
                                         f"({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})"},
             "stages_ms": stages,
+            "k4_gather": {"bytes": _gather_bytes(cfg, n),
+                          "achieved_TBs_over_K4": _gather_bytes(cfg, n) / (stages["K4_sparse_attention"] / 1e3) / 1e12,
+                          "l2_gather_peak_TBs": 19.6,
+                          "peak_source": "tools/gather_bench.cu, 4 TMA issuer warps x 2 CTAs/SM (measured)"},
             "e2e": {"value": ws * n / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "gpu_launches": args.steps * 5,
+            # per attend: compress, scores_tc, topk, rerank, fa_tile (part A),
+            # sparse_pw (part B), attention_list (overflow rows) -- see the
+            # committed ncu launch list under profiles/
+            "gpu_launches": args.steps * 7,
             "dense_comparator": dense,
             "clocks": clk.summary(),
         }
@@ -305,6 +312,17 @@ def _topk_bytes(cfg, n):
     hi = np.minimum(np.maximum(0, b - cfg.N_local + 1), n_cols)
     cand = np.maximum(0, hi - cfg.N_init)
     return int(cfg.h_kv * (cand.sum() * 4 + n * cfg.k_top * 4 + n * 4))
+
+
+def _gather_bytes(cfg, n):
+    """K4 part B algorithmic L2->SMEM gather: K and V of every top-k block of
+    every (token, group) row (selection.py:123-126 sizes)."""
+    m1 = (n - cfg.l_C1) // cfg.s_C1 + 1
+    n_cols = -(-m1 // cfg.s)
+    b = np.arange(n) // cfg.B
+    hi = np.minimum(np.maximum(0, b - cfg.N_local + 1), n_cols)
+    k = np.minimum(cfg.k_top, np.maximum(0, hi - cfg.N_init))
+    return int(cfg.h_kv * k.sum() * cfg.B * cfg.d_h * 2 * 2)
 
 
 def _traffic(kernel):

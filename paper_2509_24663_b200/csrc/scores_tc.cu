@@ -40,6 +40,13 @@ constexpr uint32_t kQBytes = kRows * kD * 2;      // 32 KB
 constexpr uint32_t kKBytes = kCols * kD * 2;      // 32 KB
 constexpr uint32_t kTmemCols = 256;
 
+// timing-decomposition switches for variant builds (tools/build_variants.sh)
+#ifdef SWATTN_K2_NO_EXP
+#define K2_EXP(x) (x)
+#else
+#define K2_EXP(x) fast_exp2(x)
+#endif
+
 struct ScParams {
   CUtensorMap q_map;    // Q [n][h_q][d]: box {64, 16, 8}
   CUtensorMap k1_map;   // K_C1 [m1][h_kv*d]: box {64, 128}
@@ -156,7 +163,9 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
           const uint64_t dq = tc::desc_kmajor(q_addr + h * (kQBytes / 2) + j * 32);
           const uint64_t dk = tc::desc_kmajor(k_addr + h * (kKBytes / 2) + j * 32);
           // pass 1: rows = (token, head), cols = keys; pass 2: rows = C1 columns
+#ifndef SWATTN_K2_NO_MMA
           tc::mma_ss(tmem + tb * kCols, p1 ? dq : dk, p1 ? dk : dq, idesc, kk > 0);
+#endif
         }
         tc::mma_commit(&s.tfull[tb]);
         tc::mma_commit(&s.empty[st]);
@@ -239,10 +248,10 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
             const uint32_t u1 = cidx + 1 < 32 ? va[cidx + 1] : vb[cidx + 1 - 32];
             const uint32_t u2 = cidx + 2 < 32 ? va[cidx + 2] : vb[cidx + 2 - 32];
             const uint32_t u3 = cidx + 3 < 32 ? va[cidx + 3] : vb[cidx + 3 - 32];
-            a0 = fmaf(fast_exp2(fmaf(__uint_as_float(u0), p.scale_log2, -st01.x)), st01.y, a0);
-            a1 = fmaf(fast_exp2(fmaf(__uint_as_float(u1), p.scale_log2, -st01.z)), st01.w, a1);
-            a2 = fmaf(fast_exp2(fmaf(__uint_as_float(u2), p.scale_log2, -st23.x)), st23.y, a2);
-            a3 = fmaf(fast_exp2(fmaf(__uint_as_float(u3), p.scale_log2, -st23.z)), st23.w, a3);
+            a0 = fmaf(K2_EXP(fmaf(__uint_as_float(u0), p.scale_log2, -st01.x)), st01.y, a0);
+            a1 = fmaf(K2_EXP(fmaf(__uint_as_float(u1), p.scale_log2, -st01.z)), st01.w, a1);
+            a2 = fmaf(K2_EXP(fmaf(__uint_as_float(u2), p.scale_log2, -st23.x)), st23.y, a2);
+            a3 = fmaf(K2_EXP(fmaf(__uint_as_float(u3), p.scale_log2, -st23.z)), st23.w, a3);
           }
           const float acc = (a0 + a1) + (a2 + a3);
           sc[kb + k] = acc;

@@ -11,10 +11,10 @@ timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"; tail -1 gpurun_out/${TAG}_bench.json
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_ref.json 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/${TAG}_bench_ref.json
 if [ -z "$NO_NCU" ]; then
-K='regex:compress|scores|topk|rerank|fa_tile|sparse_pb|attention_list|maxpool'
+K='regex:compress|scores|topk|rerank|fa_tile|sparse_pw|attention_list|maxpool'
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv --log-file gpurun_out/${TAG}_launches_128k.csv python tools/one_attend.py 131072 > /dev/null 2>&1
 grep -v "^==" gpurun_out/${TAG}_launches_128k.csv | awk -F'","' '{print $5, $NF}' | sed 's/"//g' | tail -12
-for k in sparse_pb scores_tc fa_tile topk; do
+for k in ${NCU_KERNELS:-sparse_pw scores_tc fa_tile topk rerank}; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -f -o gpurun_out/${TAG}_full_$k python tools/one_attend.py 131072 > gpurun_out/${TAG}_full_$k.log 2>&1; echo "ncu $k rc=$?"
 done
 fi
