@@ -142,6 +142,31 @@ int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, co
                       void *O, float *lse, int32_t *mode_taken, void *workspace,
                       size_t workspace_bytes, void *stream);
 
+/* ---- row ranges (copy-overlapped chunked prefill) ----
+ * The same computations restricted to query rows [r0, r1) of an n-token
+ * sequence: r0 and r1 are multiples of B (r1 may equal n).  Rows only read
+ * their own Q rows and K/V rows < r1, so a caller can stream Q in chunks
+ * and overlap host<->device copies with compute.  The call covering r0 == 0
+ * also builds the compressed keys of all n tokens into the workspace (K must
+ * be complete then); later ranges of the same sequence reuse them.  No
+ * reference counterpart: the reference processes whole arrays
+ * (selection.py:354-383, sparse.py:43-98); outputs are identical to the
+ * whole-sequence calls row for row. */
+int32_t swattn_select_blocks_rows(const swattn_config *cfg, const void *Q, const void *K,
+                                  int64_t n, int64_t r0, int64_t r1, int32_t mode,
+                                  int32_t *topk, int32_t *topk_cnt, int32_t *n_reranked,
+                                  void *workspace, size_t workspace_bytes, void *stream);
+int32_t swattn_sparse_fwd_rows(const swattn_config *cfg, const void *Q, const void *K,
+                               const void *V, int64_t n, int64_t r0, int64_t r1,
+                               const int32_t *topk, const int32_t *topk_cnt, void *O,
+                               float *lse, void *workspace, size_t workspace_bytes,
+                               void *stream);
+/* sparse branch of attend over rows [r0, r1) (workspace as swattn_attend) */
+int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *K,
+                           const void *V, int64_t n, int64_t r0, int64_t r1,
+                           int32_t select_mode, void *O, float *lse, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* ---- decode over a paged KV cache (K6; semantics = last row of attend) ----
  * Paged layout: page = B tokens; k_pages/v_pages [num_pages, B, h_kv, d_h]
  * bf16; block_table [batch, max_pages] int32; seq_lens [batch] int32 = tokens

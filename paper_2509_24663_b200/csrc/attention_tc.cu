@@ -48,7 +48,8 @@ struct FaParams {
   CUtensorMap v_map;
   int64_t n;
   int h_q, h_kv;
-  int n_tiles;         // token tiles of 8
+  int n_tiles;         // token tiles of 8 in this launch
+  int tile_end;        // tiles [tile_end - n_tiles, tile_end)
   int mode;            // 0 dense causal, 1 dense non-causal, 2 sparse part A
   int N_init, N_local;
   float scale_log2;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
   FaSmem &s = *reinterpret_cast<FaSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heavy (late) tiles first: causal work grows with the token index
-  const int tile = p.n_tiles - 1 - (int)blockIdx.x;
+  const int tile = p.tile_end - 1 - (int)blockIdx.x;
   const int g = blockIdx.y;
   const int64_t t0 = (int64_t)tile * kTokTile;
   const int b = (int)(t0 / kBlk);
@@ -320,8 +321,9 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
 bool attention_tc_available() { return true; }
 
 static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                         int64_t n, int mode, void *O, float *lse, float *m_out, float *l_out,
-                         cudaStream_t stream) {
+                         int64_t n, int64_t r0, int64_t r1, int mode, void *O, float *lse,
+                         float *m_out, float *l_out, cudaStream_t stream) {
+  if (r1 <= r0) return SWATTN_OK;
   FaParams p;
   memset(&p, 0, sizeof(p));
   {
@@ -346,7 +348,9 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   p.n = n;
   p.h_q = cfg->h_q;
   p.h_kv = cfg->h_kv;
-  p.n_tiles = (int)cdiv(n, kTokTile);
+  // row ranges are multiples of the 8-token tile (the last one may end at n)
+  p.tile_end = (int)cdiv(r1, kTokTile);
+  p.n_tiles = p.tile_end - (int)(r0 / kTokTile);
   p.mode = mode;
   p.N_init = cfg->N_init;
   p.N_local = cfg->N_local;
@@ -369,13 +373,13 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
 
 int32_t launch_dense_tc(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
-  return launch_fa(cfg, Q, K, V, n, causal ? 0 : 1, O, lse, nullptr, nullptr, stream);
+  return launch_fa(cfg, Q, K, V, n, 0, n, causal ? 0 : 1, O, lse, nullptr, nullptr, stream);
 }
 
 int32_t launch_sparse_part_a(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                             int64_t n, void *O, float *lse, float *m_out, float *l_out,
-                             cudaStream_t stream) {
-  return launch_fa(cfg, Q, K, V, n, 2, O, lse, m_out, l_out, stream);
+                             int64_t n, int64_t r0, int64_t r1, void *O, float *lse, float *m_out,
+                             float *l_out, cudaStream_t stream) {
+  return launch_fa(cfg, Q, K, V, n, r0, r1, 2, O, lse, m_out, l_out, stream);
 }
 
 }  // namespace swattn

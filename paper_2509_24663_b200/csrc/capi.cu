@@ -31,13 +31,15 @@ int32_t launch_compress(const swattn_config *, const void *, int64_t, void *, vo
 int32_t launch_scores_simt(const swattn_config *, const void *, const void *, const void *, int64_t,
                            int32_t, float *, int64_t, uint64_t *, int64_t, cudaStream_t);
 int32_t launch_scores_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
-                         int32_t, float *, int64_t, uint64_t *, int64_t, cudaStream_t);
+                         int64_t, int64_t, int32_t, float *, int64_t, uint64_t *, int64_t,
+                         cudaStream_t);
 int32_t launch_shared_scores(const swattn_config *, const void *, const void *, const void *,
                              int64_t, int32_t, float *, uint8_t *, float *, cudaStream_t);
 int32_t launch_maxpool(const swattn_config *, const float *, int64_t, float *, int64_t,
                        cudaStream_t);
-int32_t launch_topk(const swattn_config *, const float *, int64_t, int64_t, int32_t *, int32_t *,
-                    int32_t *, int32_t *, int32_t, const uint64_t *, int64_t, cudaStream_t);
+int32_t launch_topk(const swattn_config *, const float *, int64_t, int64_t, int64_t, int64_t,
+                    int32_t *, int32_t *, int32_t *, int32_t *, int32_t, const uint64_t *, int64_t,
+                    cudaStream_t);
 int32_t launch_rerank(const swattn_config *, const void *, const void *, const void *, int64_t,
                       int32_t, const float *, int64_t, const int32_t *, const int32_t *, int32_t,
                       int32_t *, int, cudaStream_t);
@@ -45,9 +47,11 @@ int32_t launch_attention_simt(const swattn_config *, const void *, const void *,
                               int64_t, const int32_t *, const int32_t *, int, int, void *, float *,
                               int *, cudaStream_t);
 int32_t launch_sparse_part_a(const swattn_config *, const void *, const void *, const void *,
-                             int64_t, void *, float *, float *, float *, cudaStream_t);
+                             int64_t, int64_t, int64_t, void *, float *, float *, float *,
+                             cudaStream_t);
 int32_t launch_sparse_part_b(const swattn_config *, const void *, const void *, const void *,
-                             int64_t, const int32_t *, const int32_t *, const float *,
+                             int64_t, int64_t, int64_t, const int32_t *, const int32_t *,
+                             const float *,
                              const float *, void *, float *, int32_t *, int32_t *, int,
                              cudaStream_t);
 int32_t launch_attention_list(const swattn_config *, const void *, const void *, const void *,
@@ -246,7 +250,7 @@ int32_t swattn_block_scores(const swattn_config *cfg, const void *Q, const void 
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (use_tc_scores())
-    return launch_scores_tc(cfg, Q, kc1, kc2, n, mode, s_cmp, ld, flags, L.ld_f, st);
+    return launch_scores_tc(cfg, Q, kc1, kc2, n, 0, n, mode, s_cmp, ld, flags, L.ld_f, st);
   return launch_scores_simt(cfg, Q, kc1, kc2, n, mode, s_cmp, ld, flags, L.ld_f, st);
 }
 
@@ -274,19 +278,47 @@ int32_t swattn_topk_blocks(const swattn_config *cfg, const float *s_cmp, int64_t
                            int32_t *topk, int32_t *topk_cnt, void *stream) {
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;
-  return launch_topk(cfg, s_cmp, ld, n, topk, topk_cnt, nullptr, nullptr, 0, nullptr, 0,
+  return launch_topk(cfg, s_cmp, ld, n, 0, n, topk, topk_cnt, nullptr, nullptr, 0, nullptr, 0,
                      static_cast<cudaStream_t>(stream));
 }
 
-int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void *K, int64_t n,
-                             int32_t mode, int32_t *topk, int32_t *topk_cnt, int32_t *n_reranked,
-                             void *workspace, size_t workspace_bytes, void *stream) {
-  int32_t rc = swattn_validate_config(cfg);
-  if (rc) return rc;
+}  // extern "C"
+
+namespace swattn {
+
+// Row ranges of the chunked (copy-overlapped) pipeline start on a query-block
+// boundary and end on one or at n, so no 8-token tile or 64-token query block
+// straddles two calls.
+static int32_t check_rows(const swattn_config *cfg, int64_t n, int64_t r0, int64_t r1) {
   if (n < 1) {
     set_error("empty sequence: n must be >= 1");
     return SWATTN_EINVAL;
   }
+  if (r0 < 0 || r1 > n || r0 >= r1 || r0 % cfg->B != 0 || (r1 % cfg->B != 0 && r1 != n)) {
+    set_error("row range [%lld, %lld) must satisfy 0 <= r0 < r1 <= n=%lld on multiples of B=%d",
+              (long long)r0, (long long)r1, (long long)n, cfg->B);
+    return SWATTN_EINVAL;
+  }
+  return SWATTN_OK;
+}
+
+static int32_t memset_rows(void *base, int64_t n, int h_kv, int64_t r0, int64_t r1, size_t row_bytes,
+                           int value, cudaStream_t st) {
+  for (int g = 0; g < h_kv; ++g) {
+    char *p = static_cast<char *>(base) + ((size_t)g * n + r0) * row_bytes;
+    int32_t rc = cuda_check(cudaMemsetAsync(p, value, (size_t)(r1 - r0) * row_bytes, st), "memset(rows)");
+    if (rc) return rc;
+  }
+  return SWATTN_OK;
+}
+
+static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *K, int64_t n,
+                           int64_t r0, int64_t r1, int32_t mode, int32_t *topk, int32_t *topk_cnt,
+                           int32_t *n_reranked, void *workspace, size_t workspace_bytes,
+                           cudaStream_t st) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if ((rc = check_rows(cfg, n, r0, r1))) return rc;
   if (mode < 0 || mode > 2) {
     set_error("unknown selection mode %d", mode);
     return SWATTN_EINVAL;
@@ -296,7 +328,7 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, L.total);
     return SWATTN_EINVAL;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool full = r0 == 0 && r1 == n;
   char *ws = static_cast<char *>(workspace);
   void *kc1 = ws + L.off_kc1;
   void *kc2 = ws + L.off_kc2;
@@ -304,18 +336,22 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
   uint64_t *flags = reinterpret_cast<uint64_t *>(ws + L.off_flags);
   int32_t *count = reinterpret_cast<int32_t *>(ws + L.off_count);
   int32_t *rows = reinterpret_cast<int32_t *>(ws + L.off_rows);
-  if ((rc = launch_compress(cfg, K, n, kc1, kc2, st))) return rc;
+  // the compressed keys of the whole sequence are built by the call that
+  // covers row 0 and stay in the workspace for the later row ranges
+  if (r0 == 0 && (rc = launch_compress(cfg, K, n, kc1, kc2, st))) return rc;
   if (cfg->k_top == 0 || L.n_cols <= cfg->N_init) {
-    if (cfg->k_top > 0) {
-      // no row has candidates: all-empty top-k lists
-      if ((rc = cuda_check(cudaMemsetAsync(topk, 0xff, (size_t)cfg->h_kv * n * cfg->k_top * 4, st),
-                           "memset(topk)")))
-        return rc;
-    }
-    if ((rc = cuda_check(cudaMemsetAsync(topk_cnt, 0, (size_t)cfg->h_kv * n * 4, st), "memset")))
+    if (cfg->k_top > 0 &&
+        (rc = memset_rows(topk, n, cfg->h_kv, r0, r1, (size_t)cfg->k_top * 4, 0xff, st)))
       return rc;
+    if ((rc = memset_rows(topk_cnt, n, cfg->h_kv, r0, r1, 4, 0, st))) return rc;
     if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
     return SWATTN_OK;
+  }
+  if (L.generic || !use_tc_scores()) {
+    if (!full) {
+      set_error("row ranges need the paper profile on the tensor-core path");
+      return SWATTN_EUNSUPPORTED;
+    }
   }
   if (L.generic) {
     // any-profile path: full S^shared, max-pool, top-k (no float64 boundary pass)
@@ -323,18 +359,19 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
     float *lse = reinterpret_cast<float *>(ws + L.off_lse);
     if ((rc = launch_shared_scores(cfg, Q, kc1, kc2, n, mode, shared, nullptr, lse, st))) return rc;
     if ((rc = launch_maxpool(cfg, shared, n, scmp, L.ld, st))) return rc;
-    rc = launch_topk(cfg, scmp, L.ld, n, topk, topk_cnt, nullptr, nullptr, 0, nullptr, 0, st);
+    rc = launch_topk(cfg, scmp, L.ld, n, 0, n, topk, topk_cnt, nullptr, nullptr, 0, nullptr, 0, st);
     if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
     return rc;
   }
   if (use_tc_scores())
-    rc = launch_scores_tc(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
+    rc = launch_scores_tc(cfg, Q, kc1, kc2, n, r0, r1, mode, scmp, L.ld, flags, L.ld_f, st);
   else
     rc = launch_scores_simt(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
   if (rc) return rc;
   if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset(count)"))) return rc;
   const int32_t cap = (int32_t)((int64_t)cfg->h_kv * n);
-  if ((rc = launch_topk(cfg, scmp, L.ld, n, topk, topk_cnt, count, rows, cap, flags, L.ld_f, st)))
+  if ((rc = launch_topk(cfg, scmp, L.ld, n, r0, r1, topk, topk_cnt, count, rows, cap, flags,
+                        L.ld_f, st)))
     return rc;
   if ((rc = launch_rerank(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, count, rows, cap, topk, num_sms(),
                           st)))
@@ -345,20 +382,17 @@ int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void
   return SWATTN_OK;
 }
 
-int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                          int64_t n, const int32_t *topk, const int32_t *topk_cnt, void *O,
-                          float *lse, void *workspace, size_t workspace_bytes, void *stream) {
+static int32_t sparse_rows(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                           int64_t n, int64_t r0, int64_t r1, const int32_t *topk,
+                           const int32_t *topk_cnt, void *O, float *lse, void *workspace,
+                           size_t workspace_bytes, cudaStream_t st) {
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;
-  if (n < 1) {
-    set_error("empty sequence: n must be >= 1");
-    return SWATTN_EINVAL;
-  }
+  if ((rc = check_rows(cfg, n, r0, r1))) return rc;
   if (cfg->h_q != kG * cfg->h_kv || cfg->d_h != kD) {
     set_error("unsupported profile for the attention kernels (need G=16, d_h=128)");
     return SWATTN_EUNSUPPORTED;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (use_tc_attention() && swattn_profile_supported(cfg)) {
     const size_t need = swattn_sparse_workspace_bytes(cfg, n);
     if (workspace == nullptr || workspace_bytes < need) {
@@ -371,15 +405,53 @@ int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K
     int32_t *slow_count = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4));
     int32_t *slow_list = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4) +
                                                      align_up(16));
-    if ((rc = launch_sparse_part_a(cfg, Q, K, V, n, O, lse, m_a, l_a, st))) return rc;
+    if ((rc = launch_sparse_part_a(cfg, Q, K, V, n, r0, r1, O, lse, m_a, l_a, st))) return rc;
     if ((rc = cuda_check(cudaMemsetAsync(slow_count, 0, 4, st), "memset(slow)"))) return rc;
-    if ((rc = launch_sparse_part_b(cfg, Q, K, V, n, topk, topk_cnt, m_a, l_a, O, lse, slow_count,
-                                   slow_list, num_sms(), st)))
+    if ((rc = launch_sparse_part_b(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, m_a, l_a, O, lse,
+                                   slow_count, slow_list, num_sms(), st)))
       return rc;
     return launch_attention_list(cfg, Q, K, V, n, topk, topk_cnt, slow_count, slow_list, O, lse,
                                  num_sms(), st);
   }
+  if (r0 != 0 || r1 != n) {
+    set_error("row ranges need the paper profile on the tensor-core path");
+    return SWATTN_EUNSUPPORTED;
+  }
   return launch_attention_simt(cfg, Q, K, V, n, topk, topk_cnt, 1, 1, O, lse, nullptr, st);
+}
+
+}  // namespace swattn
+
+extern "C" {
+
+int32_t swattn_select_blocks(const swattn_config *cfg, const void *Q, const void *K, int64_t n,
+                             int32_t mode, int32_t *topk, int32_t *topk_cnt, int32_t *n_reranked,
+                             void *workspace, size_t workspace_bytes, void *stream) {
+  return select_rows(cfg, Q, K, n, 0, n, mode, topk, topk_cnt, n_reranked, workspace,
+                     workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_select_blocks_rows(const swattn_config *cfg, const void *Q, const void *K, int64_t n,
+                                  int64_t r0, int64_t r1, int32_t mode, int32_t *topk,
+                                  int32_t *topk_cnt, int32_t *n_reranked, void *workspace,
+                                  size_t workspace_bytes, void *stream) {
+  return select_rows(cfg, Q, K, n, r0, r1, mode, topk, topk_cnt, n_reranked, workspace,
+                     workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                          int64_t n, const int32_t *topk, const int32_t *topk_cnt, void *O,
+                          float *lse, void *workspace, size_t workspace_bytes, void *stream) {
+  return sparse_rows(cfg, Q, K, V, n, 0, n, topk, topk_cnt, O, lse, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_sparse_fwd_rows(const swattn_config *cfg, const void *Q, const void *K,
+                               const void *V, int64_t n, int64_t r0, int64_t r1,
+                               const int32_t *topk, const int32_t *topk_cnt, void *O, float *lse,
+                               void *workspace, size_t workspace_bytes, void *stream) {
+  return sparse_rows(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, O, lse, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
 }
 
 int32_t swattn_dense_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
@@ -433,6 +505,31 @@ int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, co
               align_up((size_t)cfg->h_kv * n * 4);
   return swattn_sparse_fwd(cfg, Q, K, V, n, topk, cnt, O, lse, sws,
                            swattn_sparse_workspace_bytes(cfg, n), stream);
+}
+
+int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                           int64_t n, int64_t r0, int64_t r1, int32_t select_mode, void *O,
+                           float *lse, void *workspace, size_t workspace_bytes, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  const SelectLayout L = select_layout(cfg, n);
+  const size_t need = swattn_workspace_bytes(cfg, n);
+  if (workspace == nullptr || workspace_bytes < need) {
+    set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
+    return SWATTN_EINVAL;
+  }
+  char *ws = static_cast<char *>(workspace);
+  int32_t *topk = reinterpret_cast<int32_t *>(ws + align_up(L.total));
+  int32_t *cnt = reinterpret_cast<int32_t *>(ws + align_up(L.total) +
+                                             align_up((size_t)cfg->h_kv * n * cfg->k_top * 4));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = select_rows(cfg, Q, K, n, r0, r1, select_mode, topk, cnt, nullptr, workspace, L.total,
+                        st)))
+    return rc;
+  char *sws = ws + align_up(L.total) + align_up((size_t)cfg->h_kv * n * cfg->k_top * 4) +
+              align_up((size_t)cfg->h_kv * n * 4);
+  return sparse_rows(cfg, Q, K, V, n, r0, r1, topk, cnt, O, lse, sws,
+                     swattn_sparse_workspace_bytes(cfg, n), st);
 }
 
 }  // extern "C"

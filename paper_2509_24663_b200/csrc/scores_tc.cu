@@ -21,6 +21,8 @@
 // per row (bench.py:144-155).
 #include <string.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tc.cuh"
 #include "tma_host.cuh"
@@ -57,7 +59,8 @@ struct ScParams {
   int N_init, N_local, B, n_cols;
   int approx;
   float scale_log2;
-  int64_t tok0;
+  int64_t tok0;         // first token of the launch (>= first token with candidates)
+  int64_t r1;           // rows [tok0, r1) are computed
   int n_tiles_tok;      // CTAs along tokens
   float *s_cmp;
   int64_t ld;
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
   const int tt = p.n_tiles_tok - 1 - (int)blockIdx.x;
   const int g = blockIdx.y;
   const int64_t i0 = p.tok0 + (int64_t)tt * kTok;
-  const int64_t i_last = min(i0 + kTok - 1, p.n - 1);
+  const int64_t i_last = min(i0 + kTok - 1, p.r1 - 1);
   const int b = (int)(i0 / p.B);
   const int hi = cand_hi(b, p.N_local, p.n_cols);
   const int n_t2 = (hi + kTileBlocks - 1) / kTileBlocks;  // pass-2 tiles
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     // ---------------- pass 1: thread = row (token r/16, head r%16)
-    const int64_t my_tok = min(i0 + r / kG, p.n - 1);
+    const int64_t my_tok = min(i0 + r / kG, p.r1 - 1);
     const int64_t my_vis = use_c2 ? vis_count(my_tok, p.l_C2, p.s_C2) : vis_count(my_tok, p.l_C1, p.s_C1);
     float m = -INFINITY, l = 0.f;
     for (int u = 0; u < n_c1; ++u) {
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       for (int kk = 0; kk < 2; ++kk) {
         const int k = quad + 4 * kk;
         const int64_t tok = i0 + k;
-        const bool ok = blk_ok && tok < p.n;
+        const bool ok = blk_ok && tok < p.r1;
         float v[kPoolL];
 #pragma unroll
         for (int e = 0; e < kPoolL; ++e) v[e] = s.sc[k][min(qb * kPoolS + e, kCols - 1)];
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
           const bool R = ok && v[0] * f < v[4] && v[1] * f < v[4] && v[2] * f < v[4] && v[3] * f < v[4];
           const unsigned lm = __ballot_sync(0xffffffffu, L);
           const unsigned rm = __ballot_sync(0xffffffffu, R);
-          if (lane == 0 && tok < p.n)
+          if (lane == 0 && tok < p.r1)
             p.flags[((int64_t)g * p.n + tok) * p.ld_f + t] = spread_bits(lm) | (spread_bits(rm) << 1);
         }
       }
@@ -303,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
 bool scores_tc_available() { return true; }
 
 int32_t launch_scores_tc(const swattn_config *cfg, const void *Q, const void *kc1, const void *kc2,
-                         int64_t n, int32_t mode, float *s_cmp, int64_t ld, uint64_t *flags,
-                         int64_t ld_f, cudaStream_t stream) {
+                         int64_t n, int64_t r0, int64_t r1, int32_t mode, float *s_cmp, int64_t ld,
+                         uint64_t *flags, int64_t ld_f, cudaStream_t stream) {
   ScParams p;
   memset(&p, 0, sizeof(p));
   p.n = n;
@@ -320,9 +323,12 @@ int32_t launch_scores_tc(const swattn_config *cfg, const void *Q, const void *kc
   p.approx = mode == SWATTN_SELECT_APPROX && p.m2 > 0;
   const float scale = cfg->scale_compressed_logits ? 1.f / sqrtf((float)cfg->d_h) : 1.f;
   p.scale_log2 = scale * 1.4426950408889634f;
-  p.tok0 = (int64_t)(cfg->N_init + cfg->N_local) * cfg->B;
-  if (p.tok0 >= n || p.n_cols <= cfg->N_init) return SWATTN_OK;
-  p.n_tiles_tok = (int)cdiv(n - p.tok0, kTok);
+  // rows before (N_init + N_local) * B have no candidates; tiles of 8 tokens
+  // never straddle a query block (row ranges are multiples of 8)
+  p.tok0 = std::max<int64_t>((int64_t)(cfg->N_init + cfg->N_local) * cfg->B, r0);
+  p.r1 = r1;
+  if (p.tok0 >= r1 || p.n_cols <= cfg->N_init) return SWATTN_OK;
+  p.n_tiles_tok = (int)cdiv(r1 - p.tok0, kTok);
   p.s_cmp = s_cmp;
   p.ld = ld;
   p.flags = flags;

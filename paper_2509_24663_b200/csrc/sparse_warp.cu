@@ -66,8 +66,8 @@ struct PwParams {
   CUtensorMap v_map;
   int64_t n;
   int h_q, h_kv, k_top;
-  int64_t tok0;        // first token with top-k blocks
-  int64_t n_items;     // h_kv * (n - tok0)
+  int64_t tok0, tok1;  // tokens [tok0, tok1) of this launch (all have top-k blocks)
+  int64_t n_items;     // h_kv * (tok1 - tok0)
   const int32_t *topk, *topk_cnt;
   const float *m_a, *l_a;  // part A row statistics [n][h_q] (log2 max, sum)
   __nv_bfloat16 *O;        // in: O_A (normalised), out: final
@@ -88,7 +88,7 @@ struct __align__(1024) PwSmem {
 };
 
 __device__ __forceinline__ void item_of(const PwParams &p, int64_t it, int &g, int64_t &t) {
-  const int64_t per = p.n - p.tok0;
+  const int64_t per = p.tok1 - p.tok0;
   g = (int)(it / per);
   t = p.tok0 + it % per;
 }
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
 }  // namespace
 
 int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                             int64_t n, const int32_t *topk, const int32_t *topk_cnt,
+                             int64_t n, int64_t r0, int64_t r1, const int32_t *topk, const int32_t *topk_cnt,
                              const float *m_a, const float *l_a, void *O, float *lse,
                              int32_t *slow_count, int32_t *slow_list, int num_sms,
                              cudaStream_t stream) {
@@ -362,8 +362,10 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
   p.h_kv = cfg->h_kv;
   p.k_top = cfg->k_top;
   p.tok0 = (int64_t)(cfg->N_init + cfg->N_local) * cfg->B;
-  if (p.tok0 >= n || cfg->k_top == 0) return SWATTN_OK;
-  p.n_items = (int64_t)cfg->h_kv * (n - p.tok0);
+  if (p.tok0 < r0) p.tok0 = r0;
+  p.tok1 = r1;
+  if (p.tok0 >= r1 || cfg->k_top == 0) return SWATTN_OK;
+  p.n_items = (int64_t)cfg->h_kv * (r1 - p.tok0);
   p.topk = topk;
   p.topk_cnt = topk_cnt;
   p.m_a = m_a;

@@ -178,15 +178,17 @@ __device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, i
 }
 
 __global__ void __launch_bounds__(kWarps * 32)
-topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int h_kv, int B, int N_init,
-            int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
+topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int64_t r0, int64_t r1, int h_kv,
+            int B, int N_init, int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
             int32_t *__restrict__ topk, int32_t *__restrict__ topk_cnt, AmbList amb) {
   extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride]
   __shared__ int hist_s[kWarps * 256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kWarps + warp;  // g * n + i
-  if (row >= (int64_t)h_kv * n) return;
-  const int64_t i = row % n;
+  const int64_t per = r1 - r0;
+  const int64_t local = (int64_t)blockIdx.x * kWarps + warp;  // g * per + (i - r0)
+  if (local >= (int64_t)h_kv * per) return;
+  const int64_t i = r0 + local % per;
+  const int64_t row = (local / per) * n + i;  // g * n + i
   const int b = (int)(i / B);
   const int hi = cand_hi(b, N_local, n_cols);
   const int ncand = hi > N_init ? hi - N_init : 0;
@@ -222,9 +224,10 @@ decode_topk_kernel(const float *__restrict__ s_cmp, int64_t ld, const int32_t *_
 
 }  // namespace
 
-int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, int64_t n,
-                    int32_t *topk, int32_t *topk_cnt, int32_t *amb_count, int32_t *amb_rows,
-                    int32_t amb_cap, const uint64_t *flags, int64_t ld_f, cudaStream_t stream) {
+int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, int64_t n, int64_t r0,
+                    int64_t r1, int32_t *topk, int32_t *topk_cnt, int32_t *amb_count,
+                    int32_t *amb_rows, int32_t amb_cap, const uint64_t *flags, int64_t ld_f,
+                    cudaStream_t stream) {
   const int64_t m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
   const int n_cols = (int)(m1 ? cdiv(m1, cfg->s) : 0);
   if (n_cols - cfg->N_init > kMaxCand) {
@@ -232,15 +235,16 @@ int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, in
     return SWATTN_EUNSUPPORTED;
   }
   if (cfg->k_top <= 0) return SWATTN_OK;
-  const int64_t rows = (int64_t)cfg->h_kv * n;
+  if (r1 <= r0) return SWATTN_OK;
+  const int64_t rows = (int64_t)cfg->h_kv * (r1 - r0);
   AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
   const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
   const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
   if (smem > 40 * 1024)
     cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   topk_kernel<<<(unsigned)cdiv(rows, kWarps), kWarps * 32, smem, stream>>>(
-      s_cmp, ld, n, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols, cfg->l_C1,
-      cand_stride, topk, topk_cnt, amb);
+      s_cmp, ld, n, r0, r1, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols,
+      cfg->l_C1, cand_stride, topk, topk_cnt, amb);
   SWATTN_LAUNCH_CHECK("topk_kernel");
   return SWATTN_OK;
 }

@@ -4,6 +4,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -58,6 +59,9 @@ def attend(Q, K, V, cfg: AttentionConfig, policy: SwitchPolicy | None = None,
     if selection_mode not in _lib.SELECT_MODE:
         raise ValueError(f"unknown selection mode {selection_mode!r}")
     host = is_host(Q)
+    if host and mode == MODE_SPARSE and cfg.h_q == 16 * cfg.h_kv and d_h == 128:
+        O_h, lse_h = attend_host_chunked(Q, K, V, cfg, selection_mode)
+        return _finish(O_h, lse_h, True), mode
     Qd, Kd, Vd = (to_device_bf16(x, nm) for x, nm in ((Q, "Q"), (K, "K"), (V, "V")))
     O = torch.empty((n, h_q, d_h), dtype=torch.bfloat16, device=Qd.device)
     lse = torch.empty((n, h_q), dtype=torch.float32, device=Qd.device)
@@ -72,3 +76,108 @@ def attend(Q, K, V, cfg: AttentionConfig, policy: SwitchPolicy | None = None,
                "swattn_attend")
     assert taken.value == (1 if mode == MODE_DENSE else 2)
     return _finish(O, lse, host), mode
+
+
+def _host_bf16(x, name: str) -> torch.Tensor:
+    """Host input -> pinned contiguous bf16 torch tensor (no copy when the
+    caller already passes one)."""
+    if isinstance(x, torch.Tensor) and x.dtype == torch.bfloat16 and x.is_pinned() and x.is_contiguous():
+        return x
+    if isinstance(x, np.ndarray):
+        if x.dtype.name == "bfloat16":
+            x = torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16)
+        else:
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16)
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor or numpy array, got {type(x).__name__}")
+    return x.to(torch.bfloat16).contiguous().pin_memory()
+
+
+class _Chunked:
+    """Per-device side streams, events and device buffers of the chunked
+    host pipeline (grow-only, reused across calls)."""
+
+    _state: dict = {}
+
+    @classmethod
+    def get(cls, device, n, h_q, h_kv, d_h):
+        key = torch.device(device).index or 0
+        st = cls._state.get(key)
+        if st is None:
+            st = {"in": torch.cuda.Stream(device), "out": torch.cuda.Stream(device), "bufs": None}
+            cls._state[key] = st
+        b = st["bufs"]
+        if b is None or b["n"] < n:
+            b = {"n": n,
+                 "Q": torch.empty((n, h_q, d_h), dtype=torch.bfloat16, device=device),
+                 "K": torch.empty((n, h_kv, d_h), dtype=torch.bfloat16, device=device),
+                 "V": torch.empty((n, h_kv, d_h), dtype=torch.bfloat16, device=device),
+                 "O": torch.empty((n, h_q, d_h), dtype=torch.bfloat16, device=device),
+                 "lse": torch.empty((n, h_q), dtype=torch.float32, device=device)}
+            st["bufs"] = b
+        return st
+
+
+def chunk_rows_for(n: int, B: int) -> int:
+    """~16 chunks, each a multiple of the query block and >= 4096 rows."""
+    rows = max(4096, -(-n // 16))
+    return -(-rows // B) * B
+
+
+def attend_host_chunked(Q, K, V, cfg: AttentionConfig, selection_mode: str = "approx",
+                        out=None, chunk_rows: int | None = None, device=None):
+    """Sparse branch of attend for HOST inputs with the host<->device copies
+    overlapped with compute: K and V go over first (K1 needs all of K), then
+    Q streams in row chunks on a copy stream while the compute stream runs
+    select + sparse attention for the chunks already resident
+    (swattn_attend_rows), and a second copy stream returns O / lse of each
+    finished chunk.  Returns pinned host (O bf16 [n, h_q, d_h], lse fp32
+    [n, h_q]); `out` may pass them in.  Rows are computed exactly as by the
+    whole-sequence call."""
+    Qh, Kh, Vh = _host_bf16(Q, "Q"), _host_bf16(K, "K"), _host_bf16(V, "V")
+    n, h_q, d_h = Qh.shape
+    h_kv = Kh.shape[1]
+    device = torch.device(device or "cuda")
+    st = _Chunked.get(device, n, h_q, h_kv, d_h)
+    b = st["bufs"]
+    Qd, Kd, Vd, Od, ld = (b[k][:n] for k in ("Q", "K", "V", "O", "lse"))
+    if out is None:
+        O_h = torch.empty((n, h_q, d_h), dtype=torch.bfloat16, pin_memory=True)
+        lse_h = torch.empty((n, h_q), dtype=torch.float32, pin_memory=True)
+    else:
+        O_h, lse_h = out
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    ws = Workspace.get(L.swattn_workspace_bytes(c, n), device)
+    comp = torch.cuda.current_stream(device)
+    s_in, s_out = st["in"], st["out"]
+    rows = chunk_rows or chunk_rows_for(n, cfg.B)
+    bounds = [(r, min(n, r + rows)) for r in range(0, n, rows)]
+    s_in.wait_stream(comp)   # device buffers may still be read by the previous call
+    s_out.wait_stream(comp)
+    with torch.cuda.stream(s_in):
+        Kd.copy_(Kh, non_blocking=True)
+        Vd.copy_(Vh, non_blocking=True)
+        q_ready = []
+        for r0, r1 in bounds:
+            Qd[r0:r1].copy_(Qh[r0:r1], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(s_in)
+            q_ready.append(e)
+    sel = _lib.SELECT_MODE[selection_mode]
+    for (r0, r1), e in zip(bounds, q_ready):
+        comp.wait_event(e)
+        _lib.check(L.swattn_attend_rows(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), n, r0, r1,
+                                        sel, Od.data_ptr(), ld.data_ptr(), ws.data_ptr(),
+                                        ws.numel(), comp.cuda_stream), "swattn_attend_rows")
+        done = torch.cuda.Event()
+        done.record(comp)
+        s_out.wait_event(done)
+        with torch.cuda.stream(s_out):
+            O_h[r0:r1].copy_(Od[r0:r1], non_blocking=True)
+            lse_h[r0:r1].copy_(ld[r0:r1], non_blocking=True)
+    comp.wait_stream(s_out)
+    # the host buffers are valid once the caller's stream reaches this point
+    # (attend synchronises before handing them to Python)
+    comp.synchronize()
+    return O_h, lse_h

@@ -80,3 +80,20 @@ def test_workspace_grows_with_n():
     assert 0 < a < b
     # S^cmp candidate region dominates at 128K: h_kv * n * 2048 * 4 bytes
     assert b >= 2 * 131072 * 2048 * 4
+
+
+@pytest.mark.parametrize("r0,r1", [(-64, 64), (0, 0), (64, 32), (32, 128), (0, 100), (0, 4097)])
+def test_row_range_validation(r0, r1):
+    """swattn_attend_rows rejects ranges that are empty, out of [0, n] or not
+    on query-block boundaries, before touching any device memory."""
+    L = _lib.lib()
+    c = _lib.c_config(AttentionConfig())
+    n = 4096
+    ws = L.swattn_workspace_bytes(c, n)
+    # a fake (never dereferenced) workspace pointer large enough for the size check
+    rc = L.swattn_select_blocks_rows(c, None, None, n, r0, r1, 2, None, None, None, 1 << 40, ws, None)
+    assert rc == _lib.SWATTN_EINVAL
+    assert "row range" in _lib.last_error()
+    rc = L.swattn_sparse_fwd_rows(c, None, None, None, n, r0, r1, None, None, None, None, None,
+                                  ws, None)
+    assert rc == _lib.SWATTN_EINVAL and "row range" in _lib.last_error()

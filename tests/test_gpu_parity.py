@@ -317,3 +317,22 @@ def test_decode_incremental_append_equals_bulk():
         b.append(0, _dev(K[t:t + 1]), _dev(V[t:t + 1]))
     torch.cuda.synchronize()
     assert torch.equal(a.kc1, b.kc1) and torch.equal(a.kc2, b.kc2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,rows", [("paper_n16384_s2", 4096), ("paper_n10000_s1", 2048)])
+def test_chunked_host_pipeline_equals_whole(name, rows):
+    """attend_host_chunked (Q streamed in row chunks, copies overlapped with
+    swattn_attend_rows) reproduces the whole-sequence call bit for bit."""
+    from paper_2509_24663_b200.switch import attend_host_chunked
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load(name)
+    whole, mode = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    torch.cuda.synchronize()
+    Qh, Kh, Vh = (x.cpu().pin_memory() for x in (Qd, Kd, Vd))
+    O_h, lse_h = attend_host_chunked(Qh, Kh, Vh, cfg, "approx", chunk_rows=rows)
+    assert torch.equal(O_h, whole.output.cpu())
+    assert torch.equal(lse_h, whole.lse.cpu())
+    # and the public attend() on host arrays takes the same path
+    res, _ = attend(Q, K, V, cfg, SwitchPolicy(forced_mode="sparse"))
+    ref = whole.output.cpu().view(torch.int16).numpy().view(ml_dtypes.bfloat16)
+    assert np.array_equal(res.output.view(np.int16), ref.view(np.int16))
