@@ -43,6 +43,25 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (offloads the MUFU in exp-bound epilogues): round to
+// the nearest integer n with the 1.5*2^23 trick, 2^f on f in [-0.5, 0.5] by a
+// degree-6 Taylor polynomial (relative error <= 1.3e-7, the same class as
+// ex2.approx's 2 ulp), then add n to the exponent field.  x is clamped to
+// [-126, 127]: results below 2^-126 are returned as 2^-126 instead of 0,
+// which only matters for sums in which every term is below 1e-38.
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fminf(fmaxf(x, -126.f), 127.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = 1.5403530393381608e-4f;
+  p = fmaf(p, f, 1.3333558146428443e-3f);
+  p = fmaf(p, f, 9.6181291076284772e-3f);
+  p = fmaf(p, f, 5.5504108664821580e-2f);
+  p = fmaf(p, f, 2.4022650695910071e-1f);
+  p = fmaf(p, f, 6.9314718055994531e-1f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 // #pooled entries with span_end <= i (compression.py:89-91)
 __host__ __device__ __forceinline__ int64_t vis_count(int64_t i, int length, int stride) {
