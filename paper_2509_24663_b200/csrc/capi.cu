@@ -42,7 +42,8 @@ int32_t launch_topk(const swattn_config *, const float *, int64_t, int64_t, int6
                     cudaStream_t);
 int32_t launch_rerank(const swattn_config *, const void *, const void *, const void *, int64_t,
                       int32_t, const float *, int64_t, const int32_t *, const int32_t *, int32_t,
-                      int32_t *, int, cudaStream_t);
+                      int32_t *, void *, int, cudaStream_t);
+size_t rerank_partials_bytes();
 int32_t launch_attention_simt(const swattn_config *, const void *, const void *, const void *,
                               int64_t, const int32_t *, const int32_t *, int, int, void *, float *,
                               int *, cudaStream_t);
@@ -89,7 +90,8 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SelectLayout {
   int64_t m1, m2, n_cols, ld, ld_f;
-  size_t off_kc1, off_kc2, off_scmp, off_flags, off_count, off_rows, off_shared, off_lse, total;
+  size_t off_kc1, off_kc2, off_scmp, off_flags, off_count, off_rows, off_part, off_shared, off_lse,
+      total;
   bool generic;
 };
 
@@ -109,6 +111,7 @@ static SelectLayout select_layout(const swattn_config *cfg, int64_t n) {
   L.off_flags = o; o = align_up(o + (size_t)cfg->h_kv * n * L.ld_f * 8);
   L.off_count = o; o = align_up(o + 16);
   L.off_rows = o; o = align_up(o + (size_t)cfg->h_kv * n * 4);
+  L.off_part = o; o = align_up(o + rerank_partials_bytes());
   L.off_shared = o;
   if (L.generic) o = align_up(o + (size_t)n * cfg->h_kv * L.m1 * 4);
   L.off_lse = o;
@@ -373,8 +376,8 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
   if ((rc = launch_topk(cfg, scmp, L.ld, n, r0, r1, topk, topk_cnt, count, rows, cap, flags,
                         L.ld_f, st)))
     return rc;
-  if ((rc = launch_rerank(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, count, rows, cap, topk, num_sms(),
-                          st)))
+  if ((rc = launch_rerank(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, count, rows, cap, topk,
+                          ws + L.off_part, num_sms(), st)))
     return rc;
   if (n_reranked)
     return cuda_check(cudaMemcpyAsync(n_reranked, count, 4, cudaMemcpyDeviceToDevice, st),

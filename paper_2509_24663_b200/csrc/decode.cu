@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace swattn {
 
@@ -30,14 +31,15 @@ int32_t launch_decode_topk(const swattn_config *, const float *, int64_t, const 
 int32_t launch_rerank_decode(const swattn_config *, const void *, const void *, const void *,
                              int max_m1, int max_m2, const int32_t *seq_lens, int batch,
                              const float *, int64_t, const int32_t *, const int32_t *, int32_t,
-                             int32_t *, int, cudaStream_t);
+                             int32_t *, void *, int, cudaStream_t);
+size_t rerank_partials_bytes();
 
 namespace {
 
 constexpr int kP1Cols = 256;     // C2 columns per pass-1 CTA
 constexpr int kTileBlocks = 31;  // pass-2 tile: 31 blocks, 124 (+4) columns
 constexpr int kTileCols = 128;
-constexpr int kAttnBlocks = 8;   // visible blocks per split-KV CTA
+constexpr int kAttnBlocks = 4;   // visible blocks per split-KV warp (24 splits at batch 16)
 constexpr int kMaxSplits = 16;
 
 struct DecodeArgs {
@@ -60,25 +62,39 @@ __device__ __forceinline__ const __nv_bfloat16 *page_row(const __nv_bfloat16 *pa
   return pages + (((int64_t)page * kB + token % kB) * h_kv + g) * kD;
 }
 
-// dot of a q row held in smem (fp32) with a bf16 row in global memory
-__device__ __forceinline__ float dot_row(const float *q, const __nv_bfloat16 *k) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 4
-  for (int d = 0; d < kD; d += 8) {
-    const uint4 raw = __ldg(reinterpret_cast<const uint4 *>(k + d));
-    const __nv_bfloat162 *v = reinterpret_cast<const __nv_bfloat162 *>(&raw);
-    const float2 f0 = __bfloat1622float2(v[0]), f1 = __bfloat1622float2(v[1]);
-    const float2 f2 = __bfloat1622float2(v[2]), f3 = __bfloat1622float2(v[3]);
-    a0 = fmaf(q[d], f0.x, a0);
-    a1 = fmaf(q[d + 1], f0.y, a1);
-    a2 = fmaf(q[d + 2], f1.x, a2);
-    a3 = fmaf(q[d + 3], f1.y, a3);
-    a0 = fmaf(q[d + 4], f2.x, a0);
-    a1 = fmaf(q[d + 5], f2.y, a1);
-    a2 = fmaf(q[d + 6], f3.x, a2);
-    a3 = fmaf(q[d + 7], f3.y, a3);
+// the 16 head logits of one row, the row streamed in two 64-element halves
+// (8 x 16 B loads in flight, ~80 registers: several CTAs per SM)
+__device__ __forceinline__ void logits16(const float (*q_s)[kD], const __nv_bfloat16 *k, float (&s)[kG]) {
+#pragma unroll
+  for (int h = 0; h < kG; ++h) s[h] = 0.f;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint4 kr[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kr[i] = __ldg(reinterpret_cast<const uint4 *>(k + half * 64) + i);
+#pragma unroll
+    for (int h = 0; h < kG; ++h) {
+      const float *q = q_s[h] + half * 64;
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const __nv_bfloat162 *v = reinterpret_cast<const __nv_bfloat162 *>(&kr[i]);
+        const float4 qa = *reinterpret_cast<const float4 *>(q + 8 * i);
+        const float4 qb = *reinterpret_cast<const float4 *>(q + 8 * i + 4);
+        const float2 f0 = __bfloat1622float2(v[0]), f1 = __bfloat1622float2(v[1]);
+        const float2 f2 = __bfloat1622float2(v[2]), f3 = __bfloat1622float2(v[3]);
+        a0 = fmaf(qa.x, f0.x, a0);
+        a1 = fmaf(qa.y, f0.y, a1);
+        a0 = fmaf(qa.z, f1.x, a0);
+        a1 = fmaf(qa.w, f1.y, a1);
+        a0 = fmaf(qb.x, f2.x, a0);
+        a1 = fmaf(qb.y, f2.y, a1);
+        a0 = fmaf(qb.z, f3.x, a0);
+        a1 = fmaf(qb.w, f3.y, a1);
+      }
+      s[h] += a0 + a1;
+    }
   }
-  return (a0 + a1) + (a2 + a3);
 }
 
 // ------------------------------------------------------------ D1 append
@@ -105,7 +121,7 @@ __global__ void kcache_append_kernel(DecodeArgs a, const int32_t *prev_lens) {
 // ------------------------------------------------------------ D2 pass 1
 // grid (batch*h_kv, splits), 256 threads: thread = C2 column, 16 heads each.
 __global__ void __launch_bounds__(256) decode_pass1_kernel(DecodeArgs a, float2 *part, int splits) {
-  __shared__ float q_s[kG][kD];
+  __shared__ __align__(16) float q_s[kG][kD];
   __shared__ float2 red[8][kG];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
@@ -122,10 +138,11 @@ __global__ void __launch_bounds__(256) decode_pass1_kernel(DecodeArgs a, float2 
   for (int h = 0; h < kG; ++h) { m[h] = -INFINITY; l[h] = 0.f; }
   const int64_t c = (int64_t)blockIdx.y * kP1Cols + threadIdx.x;
   if (c < vis) {
-    const __nv_bfloat16 *kr = kc + (c * a.h_kv + g) * kD;
+    float sv[kG];
+    logits16(q_s, kc + (c * a.h_kv + g) * kD, sv);
 #pragma unroll
     for (int h = 0; h < kG; ++h) {
-      m[h] = dot_row(q_s[h], kr) * a.scale_log2;
+      m[h] = sv[h] * a.scale_log2;
       l[h] = 1.f;
     }
   }
@@ -152,9 +169,9 @@ __global__ void __launch_bounds__(256) decode_pass1_kernel(DecodeArgs a, float2 
 
 // ------------------------------------------------------------ D3 pass 2
 // grid (batch*h_kv, tiles), 128 threads: thread = C1 column of the tile.
-__global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const float2 *part,
+__global__ void __launch_bounds__(128, 4) decode_pass2_kernel(DecodeArgs a, const float2 *part,
                                                            int splits, float *s_cmp, int64_t ld) {
-  __shared__ float q_s[kG][kD];
+  __shared__ __align__(16) float q_s[kG][kD];
   __shared__ float2 stat[kG];  // (m, 1/l), log2 domain
   __shared__ float sc[kTileCols + 4];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
@@ -185,11 +202,12 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
   if (col < m1) {
     v = 0.f;
     if (col < vis1) {
-      const __nv_bfloat16 *kr = a.kc1 + (((int64_t)seq * a.max_m1 + col) * a.h_kv + g) * kD;
+      float sv[kG];
+      logits16(q_s, a.kc1 + (((int64_t)seq * a.max_m1 + col) * a.h_kv + g) * kD, sv);
       float acc = 0.f;
 #pragma unroll
       for (int h = 0; h < kG; ++h)
-        acc = fmaf(fast_exp2(dot_row(q_s[h], kr) * a.scale_log2 - stat[h].x), stat[h].y, acc);
+        acc = fmaf(fast_exp2(sv[h] * a.scale_log2 - stat[h].x), stat[h].y, acc);
       v = acc;
     }
   }
@@ -215,17 +233,55 @@ __device__ __forceinline__ int visible_block(int idx, int n_init, int ntop, cons
   return lo2 + (idx - ntop);
 }
 
-// grid (batch*h_kv, splits), 256 threads (8 warps, 2 heads each)
-__global__ void __launch_bounds__(256) decode_attn_kernel(DecodeArgs a, const int32_t *topk,
-                                                          const int32_t *topk_cnt, float *part_o,
-                                                          float2 *part_ml, int splits) {
-  __shared__ float q_s[kG][kD];
-  // rows padded by 16 B: lanes reading different key rows with 16-byte
-  // vectors hit distinct banks
-  __shared__ __align__(16) __nv_bfloat16 k_s[kB][kD + 8];
-  __shared__ __align__(16) __nv_bfloat16 v_s[kB][kD + 8];
-  __shared__ float p_s[kG][kB];
-  const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
+// ---- D5 on the tensor cores: one warp = (row, split of kAttnBlocks blocks);
+// the row's 16 query heads are the M = 16 of mma.sync.m16n8k16 (as in the
+// prefill part B, csrc/sparse_warp.cu): Q in registers, S -> P in registers,
+// O in registers, online softmax per 16-key stage.  K/V rows are gathered
+// from the page pool with cp.async into a per-warp 2-stage ring stored
+// [d half][row][64] with the 16-byte chunk XOR-swizzled by row, so the
+// ldmatrix reads are conflict-free.
+constexpr int kDW = 4;                        // warps per CTA
+constexpr int kDStageKeys = 16;
+constexpr uint32_t kDTile = kDStageKeys * kD * 2;  // 4 KB
+
+__device__ __forceinline__ uint32_t dswz(int row, int c) {  // c = 16-byte chunk 0..15
+  const int line = (c >> 3) * kDStageKeys + row;
+  return (uint32_t)(line * 128 + (((c & 7) ^ (line & 7)) << 4));
+}
+__device__ __forceinline__ void dldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2,
+                                         uint32_t &r3, bool trans) {
+  if (trans)
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+  else
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void dmma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+__global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a, const int32_t *topk,
+                                                                  const int32_t *topk_cnt,
+                                                                  float *part_o, float2 *part_ml,
+                                                                  int splits) {
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t *dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
+  auto ring = reinterpret_cast<uint8_t(*)[2][2][kDTile]>(dsm);  // [warp][stage][K|V]
+  auto qs = reinterpret_cast<__nv_bfloat16(*)[kG * kD]>(dsm + kDW * 4 * kDTile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * kDW + warp;
+  if (unit >= a.batch * a.h_kv * splits) return;
+  const int row = unit / splits, split = unit % splits;
+  const int seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
   const int64_t i = L - 1;
   const int b = (int)(i / kB);
@@ -235,88 +291,136 @@ __global__ void __launch_bounds__(256) decode_attn_kernel(DecodeArgs a, const in
   const int ntop = topk_cnt[row];
   const int nvis = n_init + ntop + (b + 1 - lo2);
   const int32_t *top = topk + (int64_t)row * a.k_top;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < kG * kD; e += blockDim.x)
-    q_s[e / kD][e % kD] = bf2f(a.q[((int64_t)seq * a.h_q + g * kG) * kD + e]);
-  // per warp: heads 2w, 2w+1; lane owns d = 4*lane..4*lane+3
-  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f}, acc[2][4] = {};
-  const int b0 = blockIdx.y * kAttnBlocks, b1 = min(nvis, b0 + kAttnBlocks);
-  for (int vi = b0; vi < b1; ++vi) {
-    const int j = visible_block(vi, n_init, ntop, top, lo2);
-    const int64_t key0 = (int64_t)j * kB;
-    const int nk = (int)min((int64_t)kB, i + 1 - key0);  // causal clip of the diagonal block
-    __syncthreads();
-    for (int e = threadIdx.x; e < kB * (kD / 8); e += blockDim.x) {
-      const int r = e / (kD / 8), c = e % (kD / 8);
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (r < nk) {
-        kv = __ldg(reinterpret_cast<const uint4 *>(page_row(a.k_pages, a.block_table, a.max_pages, seq, key0 + r, a.h_kv, g)) + c);
-        vv = __ldg(reinterpret_cast<const uint4 *>(page_row(a.v_pages, a.block_table, a.max_pages, seq, key0 + r, a.h_kv, g)) + c);
-      }
-      reinterpret_cast<uint4 *>(&k_s[r][0])[c] = kv;
-      reinterpret_cast<uint4 *>(&v_s[r][0])[c] = vv;
+  const int vb0 = split * kAttnBlocks, vb1 = min(nvis, vb0 + kAttnBlocks);
+  const int64_t pi_base = ((int64_t)row * splits + split) * kG;
+  const int h0 = lane >> 2;
+  if (vb0 >= vb1) {
+    if ((lane & 3) == 0) {
+      part_ml[pi_base + h0] = make_float2(-INFINITY, 0.f);
+      part_ml[pi_base + h0 + 8] = make_float2(-INFINITY, 0.f);
     }
-    __syncthreads();
-    // logits: warp w computes heads 2w, 2w+1 for keys lane, lane+32
+    return;
+  }
+  // q rows of the group -> smem (row-major, 256 B) -> A fragments
+  const __nv_bfloat16 *qg = a.q + ((int64_t)seq * a.h_q + g * kG) * kD;
+  for (int e = lane; e < kG * kD / 8; e += 32)
+    reinterpret_cast<uint4 *>(qs[warp])[e] = reinterpret_cast<const uint4 *>(qg)[e];
+  __syncwarp();
+  const int lm = lane >> 3, lr = lane & 7;
+  uint32_t qa[8][4];
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int h = 2 * warp + hh;
-      float s0 = -INFINITY, s1 = -INFINITY;
-      float d0 = 0.f, d1 = 0.f;
-#pragma unroll 4
-      for (int d = 0; d < kD; d += 8) {
-        const uint4 ka = *reinterpret_cast<const uint4 *>(&k_s[lane][d]);
-        const uint4 kb = *reinterpret_cast<const uint4 *>(&k_s[lane + 32][d]);
-        const __nv_bfloat162 *pa = reinterpret_cast<const __nv_bfloat162 *>(&ka);
-        const __nv_bfloat162 *pb = reinterpret_cast<const __nv_bfloat162 *>(&kb);
+  for (int ks = 0; ks < 8; ++ks) {
+    // matrices: (heads 0-7, d lo), (heads 8-15, d lo), (heads 0-7, d hi), (heads 8-15, d hi)
+    const int head = (lm & 1) * 8 + lr, d = ks * 16 + (lm >> 1) * 8;
+    const uint32_t addr = tc::smem_u32(&qs[warp][head * kD + d]);
+    dldsm_x4(addr, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], false);
+  }
+  // stage s of this warp's key stream: block vb0 + s / 4, rows (s % 4) * 16 ..
+  const int nst = (vb1 - vb0) * (kB / kDStageKeys);
+  auto issue = [&](int st_idx, int slot) {
+    const int j = visible_block(vb0 + st_idx / 4, n_init, ntop, top, lo2);
+    const int page = a.block_table[(int64_t)seq * a.max_pages + j];
+    const int r0 = (st_idx % 4) * kDStageKeys;
+    // 16 rows x 16 chunks of 16 B per tensor: 8 per lane
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 fa = __bfloat1622float2(pa[e]), fb = __bfloat1622float2(pb[e]);
-          d0 = fmaf(q_s[h][d + 2 * e], fa.x, d0);
-          d0 = fmaf(q_s[h][d + 2 * e + 1], fa.y, d0);
-          d1 = fmaf(q_s[h][d + 2 * e], fb.x, d1);
-          d1 = fmaf(q_s[h][d + 2 * e + 1], fb.y, d1);
-        }
+    for (int e = 0; e < 8; ++e) {
+      const int idx = e * 32 + lane, rr = idx >> 4, c = idx & 15;
+      const int64_t off = (((int64_t)page * kB + r0 + rr) * a.h_kv + g) * kD + c * 8;
+      const uint32_t dk = tc::smem_u32(ring[warp][slot][0]) + dswz(rr, c);
+      const uint32_t dv = tc::smem_u32(ring[warp][slot][1]) + dswz(rr, c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dk), "l"(a.k_pages + off));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dv), "l"(a.v_pages + off));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  issue(0, 0);
+  if (nst > 1) issue(1, 1);
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  float o[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  for (int s2 = 0; s2 < nst; ++s2) {
+    const int slot = s2 & 1;
+    if (s2 + 1 < nst) asm volatile("cp.async.wait_group 1;");
+    else asm volatile("cp.async.wait_group 0;");
+    __syncwarp();
+    const uint32_t kst = tc::smem_u32(ring[warp][slot][0]), vst = tc::smem_u32(ring[warp][slot][1]);
+    float sc[2][4] = {};
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t b00, b01, b10, b11;
+      dldsm_x4(kst + dswz((lm >> 1) * 8 + lr, ks * 2 + (lm & 1)), b00, b01, b10, b11, false);
+      dmma(sc[0], qa[ks], b00, b01);
+      dmma(sc[1], qa[ks], b10, b11);
+    }
+    // causal clip: keys after i (only in the diagonal block) are masked
+    const int j = visible_block(vb0 + s2 / 4, n_init, ntop, top, lo2);
+    const int64_t key0 = (int64_t)j * kB + (s2 % 4) * kDStageKeys;
+    float x[2][4];
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int jt = 0; jt < 2; ++jt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t key = key0 + jt * 8 + (lane & 3) * 2 + (e & 1);
+        const float v = key <= i ? sc[jt][e] * a.attn_scale_log2 : -INFINITY;
+        x[jt][e] = v;
+        if (e < 2) mx0 = fmaxf(mx0, v); else mx1 = fmaxf(mx1, v);
       }
-      if (lane < nk) s0 = d0 * a.attn_scale_log2;
-      if (lane + 32 < nk) s1 = d1 * a.attn_scale_log2;
-      float mx = fmaxf(s0, s1);
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float m_new = fmaxf(m[hh], mx);
-      const float alpha = (m[hh] == -INFINITY) ? 0.f : fast_exp2(m[hh] - m_new);
-      const float p0 = (lane < nk) ? fast_exp2(s0 - m_new) : 0.f;
-      const float p1 = (lane + 32 < nk) ? fast_exp2(s1 - m_new) : 0.f;
-      float ps = p0 + p1;
-      for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-      l[hh] = l[hh] * alpha + ps;
-      m[hh] = m_new;
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float al0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - mn0);
+    const float al1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[hh][e] *= alpha;
-      p_s[h][lane] = p0;
-      p_s[h][lane + 32] = p1;
+    for (int jt = 0; jt < 2; ++jt) {
+      x[jt][0] = (mn0 == -INFINITY) ? 0.f : fast_exp2(x[jt][0] - mn0);
+      x[jt][1] = (mn0 == -INFINITY) ? 0.f : fast_exp2(x[jt][1] - mn0);
+      x[jt][2] = (mn1 == -INFINITY) ? 0.f : fast_exp2(x[jt][2] - mn1);
+      x[jt][3] = (mn1 == -INFINITY) ? 0.f : fast_exp2(x[jt][3] - mn1);
+      ps0 += x[jt][0] + x[jt][1];
+      ps1 += x[jt][2] + x[jt][3];
+    }
+    l0 = l0 * al0 + ps0;
+    l1 = l1 * al1 + ps1;
+#pragma unroll
+    for (int jt = 0; jt < 16; ++jt) {
+      o[jt][0] *= al0;
+      o[jt][1] *= al0;
+      o[jt][2] *= al1;
+      o[jt][3] *= al1;
+    }
+    const uint32_t pa[4] = {pack2(x[0][0], x[0][1]), pack2(x[0][2], x[0][3]), pack2(x[1][0], x[1][1]),
+                            pack2(x[1][2], x[1][3])};
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {
+      uint32_t v00, v01, v10, v11;
+      dldsm_x4(vst + dswz((lm & 1) * 8 + lr, dp * 2 + (lm >> 1)), v00, v01, v10, v11, true);
+      dmma(o[2 * dp], pa, v00, v01);
+      dmma(o[2 * dp + 1], pa, v10, v11);
     }
     __syncwarp();
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int h = 2 * warp + hh;
-      for (int r = 0; r < nk; ++r) {
-        const float pr = p_s[h][r];
-        const __nv_bfloat162 *vr = reinterpret_cast<const __nv_bfloat162 *>(&v_s[r][4 * lane]);
-        const float2 f0 = __bfloat1622float2(vr[0]), f1 = __bfloat1622float2(vr[1]);
-        acc[hh][0] = fmaf(pr, f0.x, acc[hh][0]);
-        acc[hh][1] = fmaf(pr, f0.y, acc[hh][1]);
-        acc[hh][2] = fmaf(pr, f1.x, acc[hh][2]);
-        acc[hh][3] = fmaf(pr, f1.y, acc[hh][3]);
-      }
-    }
+    if (s2 + 2 < nst) issue(s2 + 2, slot);
   }
+  // partial row sums over the quad, then the partial state of this split
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const int dc = (lane & 3) * 2;
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    const int h = 2 * warp + hh;
-    const int64_t pi = ((int64_t)row * splits + blockIdx.y) * kG + h;
-    *reinterpret_cast<float4 *>(&part_o[pi * kD + 4 * lane]) =
-        make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
-    if (lane == 0) part_ml[pi] = make_float2(m[hh], l[hh]);
+  for (int jt = 0; jt < 16; ++jt) {
+    *reinterpret_cast<float2 *>(&part_o[(pi_base + h0) * kD + jt * 8 + dc]) = make_float2(o[jt][0], o[jt][1]);
+    *reinterpret_cast<float2 *>(&part_o[(pi_base + h0 + 8) * kD + jt * 8 + dc]) = make_float2(o[jt][2], o[jt][3]);
+  }
+  if ((lane & 3) == 0) {
+    part_ml[pi_base + h0] = make_float2(m0, l0);
+    part_ml[pi_base + h0 + 8] = make_float2(m1, l1);
   }
 }
 
@@ -388,7 +492,7 @@ static DecodeArgs make_args(const swattn_config *cfg, const swattn_paged_kv *kv,
 struct DecodeLayout {
   int p1_splits, tiles, attn_splits, max_ctx;
   int64_t ld;
-  size_t off_p1, off_scmp, off_topk, off_cnt, off_count, off_rows, off_po, off_pml, total;
+  size_t off_p1, off_scmp, off_topk, off_cnt, off_count, off_rows, off_part, off_po, off_pml, total;
 };
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -411,6 +515,7 @@ static DecodeLayout decode_layout(const swattn_config *cfg, int batch, int max_p
   D.off_cnt = o; o = al(o + rows * sizeof(int32_t));
   D.off_count = o; o = al(o + 16);
   D.off_rows = o; o = al(o + rows * sizeof(int32_t));
+  D.off_part = o; o = al(o + rerank_partials_bytes());
   D.off_po = o; o = al(o + rows * D.attn_splits * kG * kD * sizeof(float));
   D.off_pml = o; o = al(o + rows * D.attn_splits * kG * sizeof(float2));
   D.total = o;
@@ -507,11 +612,21 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
                                rows, nrows, st)))
     return rc;
   if ((rc = launch_rerank_decode(cfg, q, kv->kc1, kv->kc2, kv->max_m1, kv->max_m2, kv->seq_lens,
-                                 batch, scmp, D.ld, count, rows, nrows, topk, num_sms_dec(), st)))
+                                 batch, scmp, D.ld, count, rows, nrows, topk, ws + D.off_part,
+                                 num_sms_dec(), st)))
     return rc;
-  decode_attn_kernel<<<dim3(nrows, D.attn_splits), 256, 0, st>>>(a, topk, cnt, po, pml,
-                                                                 D.attn_splits);
-  SWATTN_LAUNCH_CHECK("decode_attn_kernel");
+  {
+    const int units = nrows * D.attn_splits;
+    const int smem = kDW * 4 * kDTile + kDW * kG * kD * 2 + 1024;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    decode_attn_mma_kernel<<<(units + kDW - 1) / kDW, kDW * 32, smem, st>>>(a, topk, cnt, po, pml,
+                                                                           D.attn_splits);
+    SWATTN_LAUNCH_CHECK("decode_attn_mma_kernel");
+  }
   decode_combine_kernel<<<nrows, 512, 0, st>>>(a, cnt, po, pml, D.attn_splits,
                                                static_cast<__nv_bfloat16 *>(o), lse);
   SWATTN_LAUNCH_CHECK("decode_combine_kernel");

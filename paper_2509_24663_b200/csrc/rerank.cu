@@ -36,7 +36,158 @@ struct RerankArgs {
   int decode;
   const int32_t *seq_lens;
   int64_t max_m1, max_m2;
+  // pass-1 partials of the row-split path (few flagged rows: decode, small
+  // chunks): [kSplitRows][kP1Split][kG] (max, sum), or nullptr
+  double2 *partials;
 };
+
+// When at most kSplitRows rows are flagged, pass 1 of each row is split over
+// kP1Split CTAs (rerank_p1_kernel) so a handful of rows -- the decode case --
+// is not serialised on one SM each; larger counts keep one CTA per row.
+constexpr int kSplitRows = 256;
+constexpr int kP1Split = 16;
+
+struct RowInfo {
+  int g;
+  int64_t i, qrow, n_cols, m1;
+  const __nv_bfloat16 *kc1, *kc2;
+};
+
+__device__ __forceinline__ RowInfo row_info(const RerankArgs &a, int row) {
+  RowInfo r;
+  r.n_cols = a.n_cols;
+  r.m1 = a.m1;
+  r.kc1 = a.kc1;
+  r.kc2 = a.kc2;
+  if (a.decode) {
+    const int seq = row / a.h_kv;
+    r.g = row % a.h_kv;
+    r.i = a.seq_lens[seq] - 1;
+    r.qrow = seq;
+    r.m1 = num_pooled(r.i + 1, a.l_C1, a.s_C1);
+    r.n_cols = r.m1 ? cdiv(r.m1, a.ps) : 0;
+    r.kc1 += (int64_t)seq * a.max_m1 * a.h_kv * kD;
+    r.kc2 += (int64_t)seq * a.max_m2 * a.h_kv * kD;
+  } else {
+    r.g = row / (int)a.n;
+    r.i = row % a.n;
+    r.qrow = r.i;
+  }
+  return r;
+}
+
+// Normaliser keys of pass 1 (selection.py:165-196, :336-348).
+__device__ __forceinline__ void pass1_keys(const RerankArgs &a, const RowInfo &r,
+                                           const __nv_bfloat16 *&kc, int64_t &vis) {
+  const int64_t vis1 = vis_count(r.i, a.l_C1, a.s_C1);
+  const int64_t vis2 = a.approx ? vis_count(r.i, a.l_C2, a.s_C2) : 0;
+  const bool use_c2 = a.approx && vis2 > 0;
+  kc = use_c2 ? r.kc2 : r.kc1;
+  vis = use_c2 ? vis2 : vis1;
+}
+
+__device__ void load_q(const RerankArgs &a, const RowInfo &r, double (*q_s)[kD]) {
+  for (int t = threadIdx.x; t < kG * kD; t += kThreads) {
+    const int h = t / kD, d = t % kD;
+    q_s[h][d] = (double)bf2f(a.Q[(r.qrow * a.h_q + r.g * kG + h) * kD + d]);
+  }
+}
+
+// float64 (max, sum) of the 16 heads over normaliser columns [c_lo, c_hi),
+// 128-column chunks staged as doubles [d][c]; thread = 4 heads x 2 columns
+// register tile (8 DFMA per 3 shared loads).  Result in mh[h], lh[h].
+__device__ void pass1_range(const RerankArgs &a, const __nv_bfloat16 *kc, int g, int64_t c_lo,
+                            int64_t c_hi, const double (*q_s)[kD], double *kc_s,
+                            double (*wm)[4], double (*wl)[4], double *mh, double *lh) {
+  const int hg = threadIdx.x / 64, cg = threadIdx.x % 64;
+  double mloc[4], lloc[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { mloc[e] = -INFINITY; lloc[e] = 0.0; }
+  for (int64_t c0 = c_lo; c0 < c_hi; c0 += kChunk) {
+    __syncthreads();
+    for (int v = threadIdx.x; v < kChunk * (kD / 8); v += kThreads) {
+      const int c = v % kChunk, d0 = (v / kChunk) * 8;
+      uint4 raw = make_uint4(0, 0, 0, 0);
+      if (c0 + c < c_hi) raw = __ldg(reinterpret_cast<const uint4 *>(kc + ((c0 + c) * a.h_kv + g) * kD + d0));
+      const __nv_bfloat16 *kv = reinterpret_cast<const __nv_bfloat16 *>(&raw);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) kc_s[(d0 + e) * kChunk + c] = (double)bf2f(kv[e]);
+    }
+    __syncthreads();
+    double acc[4][2];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[e][0] = acc[e][1] = 0.0;
+#pragma unroll 4
+    for (int d = 0; d < kD; ++d) {
+      const double2 kk = *reinterpret_cast<const double2 *>(&kc_s[d * kChunk + 2 * cg]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double qv = q_s[4 * hg + e][d];
+        acc[e][0] = fma(qv, kk.x, acc[e][0]);
+        acc[e][1] = fma(qv, kk.y, acc[e][1]);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      if (c0 + 2 * cg + cc >= c_hi) continue;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double sv = acc[e][cc] * a.scale;
+        if (sv > mloc[e]) { lloc[e] = lloc[e] * exp(mloc[e] - sv) + 1.0; mloc[e] = sv; }
+        else lloc[e] += exp(sv - mloc[e]);
+      }
+    }
+  }
+  // reduce (m, l) over the 64 threads (2 warps) sharing a head group
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    double M = mloc[e];
+    for (int o = 16; o; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+    double part = (mloc[e] == -INFINITY) ? 0.0 : lloc[e] * exp(mloc[e] - M);
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) {
+      wm[threadIdx.x >> 5][e] = M;
+      wl[threadIdx.x >> 5][e] = part;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kG) {
+    const int h = threadIdx.x, w0 = (h / 4) * 2, e = h % 4;
+    const double M = fmax(wm[w0][e], wm[w0 + 1][e]);
+    double L = 0.0;
+    for (int w = w0; w < w0 + 2; ++w)
+      if (wm[w][e] != -INFINITY) L += wl[w][e] * exp(wm[w][e] - M);
+    mh[h] = M;
+    lh[h] = L;
+  }
+  __syncthreads();
+}
+
+// pass-1 partials for the row-split path: work item = (flagged row, column slice)
+__global__ void __launch_bounds__(kThreads) rerank_p1_kernel(RerankArgs a) {
+  __shared__ double q_s[kG][kD];
+  __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
+  __shared__ double mh[kG], lh[kG];
+  extern __shared__ double kc_s[];  // [kD][kChunk]
+  const int total = min(*a.count, a.cap);
+  if (total > kSplitRows || a.partials == nullptr) return;
+  for (int w = blockIdx.x; w < total * kP1Split; w += gridDim.x) {
+    const int item = w / kP1Split, part = w % kP1Split;
+    const RowInfo r = row_info(a, a.rows[item]);
+    const __nv_bfloat16 *kc;
+    int64_t vis;
+    pass1_keys(a, r, kc, vis);
+    const int64_t len = cdiv(cdiv(vis, (int64_t)kP1Split), (int64_t)kChunk) * kChunk;
+    const int64_t lo = min((int64_t)part * len, vis), hi = min(lo + len, vis);
+    __syncthreads();
+    load_q(a, r, q_s);
+    __syncthreads();
+    pass1_range(a, kc, r.g, lo, hi, q_s, kc_s, wm, wl, mh, lh);
+    if (threadIdx.x < kG)
+      a.partials[((int64_t)item * kP1Split + part) * kG + threadIdx.x] =
+          make_double2(mh[threadIdx.x], lh[threadIdx.x]);
+  }
+}
 
 __device__ double block_reduce_max(double v, double *red) {
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -67,103 +218,45 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
   __shared__ double mscore[kMaxCluster];
   __shared__ int n_members, n_above;
 
+  __shared__ double mh[kG], lh[kG];
   const int total = min(*a.count, a.cap);
+  const bool split = total <= kSplitRows && a.partials != nullptr;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int row = a.rows[item];
-    int g;
-    int64_t i, qrow, n_cols = a.n_cols, m1 = a.m1;
-    const __nv_bfloat16 *kc1 = a.kc1, *kc2 = a.kc2;
-    if (a.decode) {
-      const int seq = row / a.h_kv;
-      g = row % a.h_kv;
-      i = a.seq_lens[seq] - 1;
-      qrow = seq;
-      m1 = num_pooled(i + 1, a.l_C1, a.s_C1);
-      n_cols = m1 ? cdiv(m1, a.ps) : 0;
-      kc1 += (int64_t)seq * a.max_m1 * a.h_kv * kD;
-      kc2 += (int64_t)seq * a.max_m2 * a.h_kv * kD;
-    } else {
-      g = row / (int)a.n;
-      i = row % a.n;
-      qrow = i;
-    }
+    const RowInfo ri = row_info(a, row);
+    const int g = ri.g;
+    const int64_t i = ri.i, n_cols = ri.n_cols, m1 = ri.m1;
+    const __nv_bfloat16 *kc1 = ri.kc1;
     const int b = (int)(i / a.B);
     const int hi = cand_hi(b, a.N_local, (int)n_cols);
     const int ncand = hi - a.N_init;
     const int k = min(a.k_top, ncand);
-    for (int t = threadIdx.x; t < kG * kD; t += kThreads) {
-      const int h = t / kD, d = t % kD;
-      q_s[h][d] = (double)bf2f(a.Q[(qrow * a.h_q + g * kG + h) * kD + d]);
-    }
     __syncthreads();
-
-    // ---- pass 1 in float64: lse over the visible normaliser columns.
-    // 128-column chunks staged as doubles [d][c]; thread = 4 heads x 2 columns
-    // register tile (8 DFMA per 3 shared loads).
+    load_q(a, ri, q_s);
+    __syncthreads();
     const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
-    const int64_t vis2 = a.approx ? vis_count(i, a.l_C2, a.s_C2) : 0;
-    const bool use_c2 = a.approx && vis2 > 0;
-    const __nv_bfloat16 *kc = use_c2 ? kc2 : kc1;
-    const int64_t vis = use_c2 ? vis2 : vis1;
-    const int hg = threadIdx.x / 64, cg = threadIdx.x % 64;
-    double mloc[4], lloc[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) { mloc[e] = -INFINITY; lloc[e] = 0.0; }
-    for (int64_t c0 = 0; c0 < vis; c0 += kChunk) {
-      __syncthreads();
-      for (int v = threadIdx.x; v < kChunk * (kD / 8); v += kThreads) {
-        const int c = v % kChunk, d0 = (v / kChunk) * 8;
-        uint4 raw = make_uint4(0, 0, 0, 0);
-        if (c0 + c < vis) raw = __ldg(reinterpret_cast<const uint4 *>(kc + ((c0 + c) * a.h_kv + g) * kD + d0));
-        const __nv_bfloat16 *kv = reinterpret_cast<const __nv_bfloat16 *>(&raw);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) kc_s[(d0 + e) * kChunk + c] = (double)bf2f(kv[e]);
-      }
-      __syncthreads();
-      double acc[4][2];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[e][0] = acc[e][1] = 0.0;
-#pragma unroll 4
-      for (int d = 0; d < kD; ++d) {
-        const double2 kk = *reinterpret_cast<const double2 *>(&kc_s[d * kChunk + 2 * cg]);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double qv = q_s[4 * hg + e][d];
-          acc[e][0] = fma(qv, kk.x, acc[e][0]);
-          acc[e][1] = fma(qv, kk.y, acc[e][1]);
+
+    // ---- pass 1 in float64: lse over the visible normaliser columns
+    if (split) {
+      if (threadIdx.x < kG) {
+        const int h = threadIdx.x;
+        double M = -INFINITY;
+        for (int pp = 0; pp < kP1Split; ++pp)
+          M = fmax(M, a.partials[((int64_t)item * kP1Split + pp) * kG + h].x);
+        double L = 0.0;
+        for (int pp = 0; pp < kP1Split; ++pp) {
+          const double2 v = a.partials[((int64_t)item * kP1Split + pp) * kG + h];
+          if (v.x != -INFINITY) L += v.y * exp(v.x - M);
         }
+        lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe (selection.py:204)
       }
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        if (c0 + 2 * cg + cc >= vis) continue;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double sv = acc[e][cc] * a.scale;
-          if (sv > mloc[e]) { lloc[e] = lloc[e] * exp(mloc[e] - sv) + 1.0; mloc[e] = sv; }
-          else lloc[e] += exp(sv - mloc[e]);
-        }
-      }
-    }
-    // reduce (m, l) over the 64 threads (2 warps) sharing a head group
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      double M = mloc[e];
-      for (int o = 16; o; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
-      double part = (mloc[e] == -INFINITY) ? 0.0 : lloc[e] * exp(mloc[e] - M);
-      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if ((threadIdx.x & 31) == 0) {
-        wm[threadIdx.x >> 5][e] = M;
-        wl[threadIdx.x >> 5][e] = part;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < kG) {
-      const int h = threadIdx.x, w0 = (h / 4) * 2, e = h % 4;
-      const double M = fmax(wm[w0][e], wm[w0 + 1][e]);
-      double L = 0.0;
-      for (int w = w0; w < w0 + 2; ++w)
-        if (wm[w][e] != -INFINITY) L += wl[w][e] * exp(wm[w][e] - M);
-      lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe (selection.py:204)
+    } else {
+      const __nv_bfloat16 *kc;
+      int64_t vis;
+      pass1_keys(a, ri, kc, vis);
+      pass1_range(a, kc, g, 0, vis, q_s, kc_s, wm, wl, mh, lh);
+      if (threadIdx.x < kG)
+        lse_s[threadIdx.x] = (mh[threadIdx.x] == -INFINITY) ? 0.0 : mh[threadIdx.x] + log(lh[threadIdx.x]);
     }
     __syncthreads();
 
@@ -275,12 +368,32 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
   }
 }
 
+int32_t run_rerank(const RerankArgs &a, int num_sms, cudaStream_t stream) {
+  const size_t smem = (size_t)kD * kChunk * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rerank_p1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (a.partials != nullptr) {
+    // no-op unless at most kSplitRows rows were flagged (decided on the device)
+    rerank_p1_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);
+    SWATTN_LAUNCH_CHECK("rerank_p1_kernel");
+  }
+  rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
+  SWATTN_LAUNCH_CHECK("rerank_kernel");
+  return SWATTN_OK;
+}
+
 }  // namespace
+
+size_t rerank_partials_bytes() { return (size_t)kSplitRows * kP1Split * kG * sizeof(double2); }
 
 int32_t launch_rerank(const swattn_config *cfg, const void *Q, const void *kc1, const void *kc2,
                       int64_t n, int32_t mode, const float *s_cmp, int64_t ld,
                       const int32_t *count, const int32_t *rows, int32_t cap, int32_t *topk,
-                      int num_sms, cudaStream_t stream) {
+                      void *partials, int num_sms, cudaStream_t stream) {
   if (cfg->k_top > kTopMax) {
     set_error("unsupported: k_top=%d exceeds the compiled bound %d", cfg->k_top, kTopMax);
     return SWATTN_EUNSUPPORTED;
@@ -312,22 +425,15 @@ int32_t launch_rerank(const swattn_config *cfg, const void *Q, const void *kc1, 
   a.decode = 0;
   a.seq_lens = nullptr;
   a.max_m1 = a.max_m2 = 0;
-  const size_t smem = (size_t)kD * kChunk * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
-  SWATTN_LAUNCH_CHECK("rerank_kernel");
-  return SWATTN_OK;
+  a.partials = static_cast<double2 *>(partials);
+  return run_rerank(a, num_sms, stream);
 }
 
 int32_t launch_rerank_decode(const swattn_config *cfg, const void *q, const void *kc1,
                              const void *kc2, int max_m1, int max_m2, const int32_t *seq_lens,
                              int batch, const float *s_cmp, int64_t ld, const int32_t *count,
-                             const int32_t *rows, int32_t cap, int32_t *topk, int num_sms,
-                             cudaStream_t stream) {
+                             const int32_t *rows, int32_t cap, int32_t *topk, void *partials,
+                             int num_sms, cudaStream_t stream) {
   RerankArgs a;
   memset(&a, 0, sizeof(a));
   a.Q = static_cast<const __nv_bfloat16 *>(q);
@@ -354,11 +460,8 @@ int32_t launch_rerank_decode(const swattn_config *cfg, const void *q, const void
   a.seq_lens = seq_lens;
   a.max_m1 = max_m1;
   a.max_m2 = max_m2;
-  const size_t smem = (size_t)kD * kChunk * sizeof(double);
-  cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
-  SWATTN_LAUNCH_CHECK("rerank_kernel(decode)");
-  return SWATTN_OK;
+  a.partials = static_cast<double2 *>(partials);
+  return run_rerank(a, num_sms, stream);
 }
 
 }  // namespace swattn
