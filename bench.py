@@ -169,13 +169,14 @@ def run_ours(args):
     from paper_2509_24663_b200.core import AttentionConfig, make_qkv
     from paper_2509_24663_b200.counts import (compress_bytes, dense_total_counts,
                                               selection_total_counts, sparse_total_counts)
+    from paper_2509_24663_b200.parallel import context_parallel_attend
     from paper_2509_24663_b200.switch import attend_host_chunked
 
     cfg = AttentionConfig()
     n = args.n
     L = _lib.lib()
     c = _lib.c_config(cfg)
-    Q, K, V = make_qkv(n, 32, 2, 128, seed=rank, device="cuda")
+    Q, K, V = make_qkv(n, 32, 2, 128, seed=0 if args.cp else rank, device="cuda")
     O_ = torch.empty_like(Q)
     lse = torch.empty((n, 32), dtype=torch.float32, device="cuda")
     wsb = L.swattn_workspace_bytes(c, n)
@@ -185,6 +186,9 @@ def run_ours(args):
     taken = _lib.ctypes.c_int32(0)
 
     def step():
+        if args.cp:
+            context_parallel_attend(Q, K, V, cfg, ws, rank, O=O_, lse=lse)
+            return
         _lib.check(L.swattn_attend(c, Q.data_ptr(), K.data_ptr(), V.data_ptr(), n, -1, 0, 2,
                                    O_.data_ptr(), lse.data_ptr(), _lib.ctypes.byref(taken),
                                    work.data_ptr(), wsb, sh), "attend")
@@ -208,7 +212,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    tokens_per_s = ws * n / (ms / 1e3)
+    tokens_per_s = (n if args.cp else ws * n) / (ms / 1e3)
 
     # ---- e2e through the public API with host buffers (H2D + D2H in the timed region)
     Qh = Q.cpu().pin_memory()
@@ -217,7 +221,17 @@ def run_ours(args):
     Oh = torch.empty(O_.shape, dtype=O_.dtype).pin_memory()
     lh = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
 
+    def e2e_step_cp():
+        # CP: each rank copies the whole sequence in, computes its rows and
+        # returns only its own O/lse rows
+        qd, kd, vd = (x.to("cuda", non_blocking=True) for x in (Qh, Kh, Vh))
+        _, _, (r0, r1) = context_parallel_attend(qd, kd, vd, cfg, ws, rank, O=O_, lse=lse)
+        Oh[r0:r1].copy_(O_[r0:r1], non_blocking=True)
+        lh[r0:r1].copy_(lse[r0:r1], non_blocking=True)
+
     def e2e_step():
+        if args.cp:
+            return e2e_step_cp()
         # the host-buffer entry point: K/V then Q chunks stream H2D on a copy
         # stream while earlier chunks compute; O/lse chunks stream back D2H
         attend_host_chunked(Qh, Kh, Vh, cfg, "approx", out=(Oh, lh))
@@ -266,12 +280,16 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong" if args.cp else "weak",
+            "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (make_qkv Philox normal(0,1), bf16)",
             "config": {"workload": f"attend (sparse branch) prefill, n={n} tokens, batch 1 per GPU",
                        "n": n, "batch_per_gpu": 1, "h_q": 32, "h_kv": 2, "d_h": 128, "B": 64,
                        "budget_blocks": "1+32+63", "selection_mode": "approx",
-                       "parallelism": f"batch x kv-group sharding, {ws} rank(s), no collective",
+                       "parallelism": (f"context parallel: one sequence, cost-balanced query rows over "
+                                       f"{ws} rank(s), K/V replicated, no data-path collective"
+                                       if args.cp else
+                                       f"batch x kv-group sharding, {ws} rank(s), no collective"),
                        "l2": "inputs larger than L2 (Q = 1 GiB), no flush"},
             "roofline": {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,
@@ -443,6 +461,9 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=48)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--cp", action="store_true",
+                    help="context parallelism: all ranks share ONE n-token sequence, each "
+                         "computes its cost-balanced query rows (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

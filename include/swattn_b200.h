@@ -161,6 +161,11 @@ int32_t swattn_sparse_fwd_rows(const swattn_config *cfg, const void *Q, const vo
                                const int32_t *topk, const int32_t *topk_cnt, void *O,
                                float *lse, void *workspace, size_t workspace_bytes,
                                void *stream);
+/* Build the compressed keys of all n tokens into an attend workspace, for a
+ * caller whose first row range does not start at 0 (context parallelism:
+ * each rank computes its own rows of one sequence). */
+int32_t swattn_attend_prepare(const swattn_config *cfg, const void *K, int64_t n,
+                              void *workspace, size_t workspace_bytes, void *stream);
 /* sparse branch of attend over rows [r0, r1) (workspace as swattn_attend) */
 int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *K,
                            const void *V, int64_t n, int64_t r0, int64_t r1,

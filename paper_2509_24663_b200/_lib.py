@@ -85,6 +85,7 @@ def lib():
         "swattn_select_blocks_rows": (I32, [cfgp, P, P, I64, I64, I64, I32, P, P, P, P, SZ, P]),
         "swattn_sparse_fwd_rows": (I32, [cfgp, P, P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
         "swattn_attend_rows": (I32, [cfgp, P, P, P, I64, I64, I64, I32, P, P, P, SZ, P]),
+        "swattn_attend_prepare": (I32, [cfgp, P, I64, P, SZ, P]),
         "swattn_kcache_append": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P]),
         "swattn_decode_step": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P, P, P, P, SZ, P]),
         "swattn_decode_workspace_bytes": (SZ, [cfgp, I32, I32]),
@@ -103,7 +104,7 @@ EXPORTED = (
     "swattn_shared_scores", "swattn_topk_blocks", "swattn_select_blocks", "swattn_sparse_fwd",
     "swattn_sparse_workspace_bytes",
     "swattn_dense_fwd", "swattn_attend", "swattn_select_blocks_rows", "swattn_sparse_fwd_rows",
-    "swattn_attend_rows", "swattn_kcache_append", "swattn_decode_step",
+    "swattn_attend_rows", "swattn_attend_prepare", "swattn_kcache_append", "swattn_decode_step",
     "swattn_decode_workspace_bytes",
 )
 

@@ -510,6 +510,23 @@ int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, co
                            swattn_sparse_workspace_bytes(cfg, n), stream);
 }
 
+int32_t swattn_attend_prepare(const swattn_config *cfg, const void *K, int64_t n, void *workspace,
+                              size_t workspace_bytes, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  const SelectLayout L = select_layout(cfg, n);
+  if (workspace == nullptr || workspace_bytes < swattn_workspace_bytes(cfg, n)) {
+    set_error("workspace too small: %zu < %zu bytes", workspace_bytes, swattn_workspace_bytes(cfg, n));
+    return SWATTN_EINVAL;
+  }
+  char *ws = static_cast<char *>(workspace);
+  return launch_compress(cfg, K, n, ws + L.off_kc1, ws + L.off_kc2, static_cast<cudaStream_t>(stream));
+}
+
 int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                            int64_t n, int64_t r0, int64_t r1, int32_t select_mode, void *O,
                            float *lse, void *workspace, size_t workspace_bytes, void *stream) {

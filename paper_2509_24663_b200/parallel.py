@@ -62,3 +62,36 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def context_parallel_attend(Qd, Kd, Vd, cfg: AttentionConfig, world: int, rank: int,
+                            selection_mode: str = "approx", O=None, lse=None):
+    """Rows of one long sequence split across ranks (context parallelism).
+
+    Every rank holds Q/K/V of the whole sequence on its device (K/V are
+    67 MB each at 128K; selected blocks reach anywhere in the past), builds
+    the compressed keys itself (K1, 0.03 ms -- cheaper than any exchange) and
+    computes the sparse branch of attend for its cost-balanced query-row
+    range with swattn_attend_rows.  Outputs are row-disjoint: rank r owns
+    O[r0:r1], lse[r0:r1]; nothing is reduced.  Returns (O, lse, (r0, r1))."""
+    import torch
+
+    from . import _lib
+    from .selection import Workspace
+    n, h_q, d_h = Qd.shape
+    r0, r1 = balanced_row_ranges(cfg, n, world)[rank]
+    O = O if O is not None else torch.empty((n, h_q, d_h), dtype=torch.bfloat16, device=Qd.device)
+    lse = lse if lse is not None else torch.empty((n, h_q), dtype=torch.float32, device=Qd.device)
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    ws = Workspace.get(L.swattn_workspace_bytes(c, n), Qd.device)
+    sh = _lib.stream_handle(Qd.device)
+    if r1 > r0:
+        if r0 > 0:
+            _lib.check(L.swattn_attend_prepare(c, Kd.data_ptr(), n, ws.data_ptr(), ws.numel(), sh),
+                       "swattn_attend_prepare")
+        _lib.check(L.swattn_attend_rows(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), n, r0, r1,
+                                        _lib.SELECT_MODE[selection_mode], O.data_ptr(),
+                                        lse.data_ptr(), ws.data_ptr(), ws.numel(), sh),
+                   "swattn_attend_rows")
+    return O, lse, (r0, r1)

@@ -336,3 +336,23 @@ def test_chunked_host_pipeline_equals_whole(name, rows):
     res, _ = attend(Q, K, V, cfg, SwitchPolicy(forced_mode="sparse"))
     ref = whole.output.cpu().view(torch.int16).numpy().view(ml_dtypes.bfloat16)
     assert np.array_equal(res.output.view(np.int16), ref.view(np.int16))
+
+
+@pytest.mark.gpu
+def test_context_parallel_ranks_reassemble_whole():
+    """Context parallelism: every rank's cost-balanced row range computed
+    with swattn_attend_prepare + swattn_attend_rows (ranks run one after the
+    other on this GPU) reassembles the whole-sequence attend bit for bit."""
+    from paper_2509_24663_b200.parallel import context_parallel_attend
+    rec, prof, cfg, _, (Qd, Kd, Vd) = _load("paper_n16384_s2")
+    whole, _ = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    for world in (2, 4):
+        O = torch.full_like(whole.output, float("nan"))
+        lse = torch.full_like(whole.lse, float("nan"))
+        covered = []
+        for rank in range(world):
+            _, _, rr = context_parallel_attend(Qd, Kd, Vd, cfg, world, rank, O=O, lse=lse)
+            covered.append(rr)
+        torch.cuda.synchronize()
+        assert covered[0][0] == 0 and covered[-1][1] == Qd.shape[0]
+        assert torch.equal(O, whole.output) and torch.equal(lse, whole.lse), world
