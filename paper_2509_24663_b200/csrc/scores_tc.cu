@@ -15,8 +15,12 @@
 //     region [N_init, min(b - N_local + 1, n_cols)) is computed and written
 //     (S^cmp fp32), plus the argmax-at-shared-column flag bits K3 uses to
 //     classify exact ties.
-// Warp roles (192 threads): warp 0 TMA (Q once; C2 chunks then C1 tiles
-// through one 2-stage ring), warp 1 MMA issuer, warps 2..5 epilogues.
+// Warp roles (320 threads): warp 0 TMA (Q once; C2 chunks then C1 tiles
+// through one 2-stage ring), warp 1 MMA issuer, warps 2..9 epilogues in two
+// warpgroups that split every TMEM tile by columns (pass 1: key columns
+// 0-63 / 64-127 of a chunk; pass 2: tokens 0-3 / 4-7), so each SM sub-
+// partition runs 4 epilogue warps (2 per CTA) and keeps MUFU busy while the
+// other warps wait on TMEM loads or the max-pool barrier.
 // Roofline: tensor + MUFU; FLOP = 2 * h_q * d * (pass-1 cols + pass-2 cols)
 // per row (bench.py:144-155).
 #include <string.h>
@@ -31,7 +35,8 @@ namespace swattn {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
+constexpr int kEpiThreads = 256;  // warps 2..9
 constexpr int kTok = 8;
 constexpr int kRows = kTok * kG;           // 128
 constexpr int kCols = 128;                 // columns per chunk / tile
@@ -73,6 +78,7 @@ struct __align__(1024) ScSmem {
   uint8_t k[kStages][kKBytes];
   uint64_t q_full, full[kStages], empty[kStages], tfull[2], tempty[2];
   __align__(16) float2 stat[kRows];  // (m, 1/l) per (token, head) row, log2 domain
+  float2 stat_hi[kRows];             // warpgroup 1's pass-1 (m, l) before the merge
   float sc[kTok][kCols + 4];   // tile column scores for the max-pool
   uint32_t tmem_base;
 };
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s.tfull[i], 1);
-      tc::mbar_init(&s.tempty[i], 128);
+      tc::mbar_init(&s.tempty[i], kEpiThreads);
     }
     tc::fence_barrier_init();
   }
@@ -176,10 +182,12 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       __syncwarp();
     }
   } else {
-    const int quad = warp & 3;
+    const int quad = warp & 3;           // TMEM lane quadrant of this warp
+    const int half = (warp - 2) >> 2;    // epilogue warpgroup 0 / 1
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    // ---------------- pass 1: thread = row (token r/16, head r%16)
+    // ---------------- pass 1: thread = row (token r/16, head r%16), key
+    // columns [64 half, 64 half + 64) of every chunk
     const int64_t my_tok = min(i0 + r / kG, p.r1 - 1);
     const int64_t my_vis = use_c2 ? vis_count(my_tok, p.l_C2, p.s_C2) : vis_count(my_tok, p.l_C1, p.s_C1);
     float m = -INFINITY, l = 0.f;
@@ -187,40 +195,46 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       const int tb = u & 1;
       tc::mbar_wait(&s.tfull[tb], (u >> 1) & 1);
       tc::tc_fence_after();
-      const int64_t c0 = (int64_t)u * kCols;
-#pragma unroll
-      for (int q = 0; q < kCols; q += 64) {
-        uint32_t va[32], vb[32];
-        tc::tmem_ld32(tmem + lane_off + tb * kCols + q, va);
-        tc::tmem_ld32(tmem + lane_off + tb * kCols + q + 32, vb);
-        tc::tmem_ld_wait();
-        float x[64];
-        float cm = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          const uint32_t u = e < 32 ? va[e] : vb[e - 32];
-          x[e] = (c0 + q + e < my_vis) ? __uint_as_float(u) * p.scale_log2 : -INFINITY;
-          cm = fmaxf(cm, x[e]);
-        }
-        if (cm > m) {
-          l *= fast_exp2(m - cm);
-          m = cm;
-        }
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          a0 += fast_exp2(x[e] - m);
-          a1 += fast_exp2(x[e + 1] - m);
-          a2 += fast_exp2(x[e + 2] - m);
-          a3 += fast_exp2(x[e + 3] - m);
-        }
-        if (m != -INFINITY) l += (a0 + a1) + (a2 + a3);
-      }
+      const int64_t c0 = (int64_t)u * kCols + half * 64;
+      uint32_t va[32], vb[32];
+      tc::tmem_ld32(tmem + lane_off + tb * kCols + half * 64, va);
+      tc::tmem_ld32(tmem + lane_off + tb * kCols + half * 64 + 32, vb);
+      tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&s.tempty[tb]);
+      float x[64];
+      float cm = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const uint32_t uu = e < 32 ? va[e] : vb[e - 32];
+        x[e] = (c0 + e < my_vis) ? __uint_as_float(uu) * p.scale_log2 : -INFINITY;
+        cm = fmaxf(cm, x[e]);
+      }
+      if (cm > m) {
+        l *= fast_exp2(m - cm);
+        m = cm;
+      }
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+      for (int e = 0; e < 64; e += 4) {
+        a0 += fast_exp2(x[e] - m);
+        a1 += fast_exp2(x[e + 1] - m);
+        a2 += fast_exp2(x[e + 2] - m);
+        a3 += fast_exp2(x[e + 3] - m);
+      }
+      if (m != -INFINITY) l += (a0 + a1) + (a2 + a3);
     }
-    s.stat[r] = make_float2(m == -INFINITY ? 0.f : m, l > 0.f ? 1.f / l : 0.f);
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    // merge the two column halves of every row
+    if (half == 1) s.stat_hi[r] = make_float2(m, l);
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+    if (half == 0) {
+      const float2 o = s.stat_hi[r];
+      const float M = fmaxf(m, o.x);
+      float L = 0.f;
+      if (M != -INFINITY) L = l * fast_exp2(m - M) + o.y * fast_exp2(o.x - M);
+      s.stat[r] = make_float2(M == -INFINITY ? 0.f : M, L > 0.f ? 1.f / L : 0.f);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 
     // ---------------- pass 2: thread = C1 column of the tile
     // No causal / edge masking is needed here: every column of a candidate
@@ -231,10 +245,10 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       const int tb = u & 1;
       tc::mbar_wait(&s.tfull[tb], (u >> 1) & 1);
       tc::tc_fence_after();
-      float sc[kTok];
-#pragma unroll
-      for (int kb = 0; kb < kTok; kb += 4) {
-        // 4 tokens x 16 heads = 64 TMEM columns per load batch, one wait
+      // this warpgroup's 4 tokens x 16 heads = 64 TMEM columns, one wait
+      float sc[4];
+      {
+        const int kb = half * 4;
         uint32_t va[32], vb[32];
         tc::tmem_ld32(tmem + lane_off + tb * kCols + kb * kG, va);
         tc::tmem_ld32(tmem + lane_off + tb * kCols + kb * kG + 32, vb);
@@ -256,25 +270,23 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
             a2 = fmaf(K2_EXP(fmaf(__uint_as_float(u2), p.scale_log2, -st23.x)), st23.y, a2);
             a3 = fmaf(K2_EXP(fmaf(__uint_as_float(u3), p.scale_log2, -st23.z)), st23.w, a3);
           }
-          const float acc = (a0 + a1) + (a2 + a3);
-          sc[kb + k] = acc;
+          sc[k] = (a0 + a1) + (a2 + a3);
         }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&s.tempty[tb]);
       // stage the tile's column scores [token][column]; the 5/4 max-pool then
-      // runs one block per lane (warp w pools tokens w and w+4), so the 31
+      // runs one block per lane (epilogue warp e pools token e), so the 31
       // block scores of a token are written coalesced and the tie flags come
       // straight out of two ballots
 #pragma unroll
-      for (int k = 0; k < kTok; ++k) s.sc[k][r] = sc[k];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int k = 0; k < 4; ++k) s.sc[half * 4 + k][r] = sc[k];
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       const int qb = lane;
       const int j = t * kTileBlocks + qb;
       const bool blk_ok = qb < kTileBlocks && j >= p.N_init && j < hi;
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        const int k = quad + 4 * kk;
+      {
+        const int k = warp - 2;
         const int64_t tok = i0 + k;
         const bool ok = blk_ok && tok < p.r1;
         float v[kPoolL];
@@ -293,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
             p.flags[((int64_t)g * p.n + tok) * p.ld_f + t] = spread_bits(lm) | (spread_bits(rm) << 1);
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // s.sc reuse by the next tile
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");  // s.sc reuse by the next tile
     }
   }
   tc::tc_fence_before();

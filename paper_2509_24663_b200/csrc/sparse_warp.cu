@@ -47,6 +47,9 @@ namespace {
 #ifndef SWATTN_PW_STAGES
 #define SWATTN_PW_STAGES 2
 #endif
+#ifndef SWATTN_PW_IPW
+#define SWATTN_PW_IPW 0  // items (tokens) per warp; 0 = persistent grid of num_sms CTAs
+#endif
 #ifndef SWATTN_PW_STAGE_KEYS
 #define SWATTN_PW_STAGE_KEYS 16
 #endif
@@ -383,7 +386,12 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
   }
   const int64_t per_cta = kWarps;
   int64_t grid = (p.n_items + per_cta - 1) / per_cta;
+#if SWATTN_PW_IPW > 0
+  // non-persistent: CTAs retire, so kernels on other streams can share SMs
+  grid = (p.n_items + per_cta * SWATTN_PW_IPW - 1) / (per_cta * SWATTN_PW_IPW);
+#else
   if (grid > num_sms) grid = num_sms;
+#endif
   sparse_pw_kernel<<<(unsigned)grid, kThreads, smem, stream>>>(p);
   SWATTN_LAUNCH_CHECK("sparse_pw_kernel");
   return SWATTN_OK;

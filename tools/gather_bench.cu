@@ -172,5 +172,26 @@ int main() {
       }
     }
   }
+  // SM-count sweep: is the gather bound per SM (ingress) or chip-level (L2)?
+  // one CTA per SM (smem forces occupancy 1), 4 issuer warps, 24 stages
+  for (int stages : {16, 24}) {
+    const int smem = stages * kTile + 1024;
+    cudaFuncSetAttribute(gather_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int grid : {sms / 4, sms / 2, (3 * sms) / 4, sms}) {
+      gather_kernel<3><<<grid, 128, smem>>>(map, base, ids, 64, stages, sink);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      gather_kernel<3><<<grid, 128, smem>>>(map, base, ids, iters, stages, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      const double gbs = (double)grid * iters * kTile / (ms * 1e6);
+      printf("SM sweep: TMA 4 issuers stages=%2d sms=%3d : %7.0f GB/s chip, %6.1f GB/s per SM\n", stages, grid,
+             gbs, gbs / grid);
+    }
+  }
   return 0;
 }
