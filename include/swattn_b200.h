@@ -56,6 +56,11 @@ enum swattn_select_mode {
   SWATTN_SELECT_FUSED_EXACT = 1,
   SWATTN_SELECT_APPROX = 2
 };
+/* OR'ed into a select mode of the row-range entry points: the compressed keys
+ * of the whole sequence are already in the workspace (written through
+ * swattn_workspace_ckeys, e.g. after an all-gather of per-rank shards), so
+ * K1 is never run, not even for a range starting at row 0. */
+#define SWATTN_SELECT_PREPARED 0x100
 
 /* attend forced modes (switch.py:27-34) */
 enum swattn_forced_mode { SWATTN_AUTO = 0, SWATTN_FORCE_DENSE = 1, SWATTN_FORCE_SPARSE = 2 };
@@ -166,6 +171,10 @@ int32_t swattn_sparse_fwd_rows(const swattn_config *cfg, const void *Q, const vo
  * each rank computes its own rows of one sequence). */
 int32_t swattn_attend_prepare(const swattn_config *cfg, const void *K, int64_t n,
                               void *workspace, size_t workspace_bytes, void *stream);
+/* Device pointers of the compressed-key slots K_C1 [m1, h_kv, d_h] and
+ * K_C2 [m2, h_kv, d_h] (bf16) inside an attend workspace for n tokens. */
+int32_t swattn_workspace_ckeys(const swattn_config *cfg, int64_t n, void *workspace,
+                               void **kc1, void **kc2);
 /* sparse branch of attend over rows [r0, r1) (workspace as swattn_attend) */
 int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *K,
                            const void *V, int64_t n, int64_t r0, int64_t r1,

@@ -22,6 +22,7 @@ SWATTN_ECUDA = 3
 SWATTN_EEMPTY = 4
 
 SELECT_MODE = {"exact": 0, "fused-exact": 1, "approx": 2}
+SELECT_PREPARED = 0x100  # compressed keys already in the workspace (swattn_b200.h)
 FORCED_MODE = {None: 0, "dense": 1, "sparse": 2}
 
 
@@ -86,6 +87,7 @@ def lib():
         "swattn_sparse_fwd_rows": (I32, [cfgp, P, P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
         "swattn_attend_rows": (I32, [cfgp, P, P, P, I64, I64, I64, I32, P, P, P, SZ, P]),
         "swattn_attend_prepare": (I32, [cfgp, P, I64, P, SZ, P]),
+        "swattn_workspace_ckeys": (I32, [cfgp, I64, P, ctypes.POINTER(P), ctypes.POINTER(P)]),
         "swattn_kcache_append": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P]),
         "swattn_decode_step": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P, P, P, P, SZ, P]),
         "swattn_decode_workspace_bytes": (SZ, [cfgp, I32, I32]),
@@ -104,7 +106,7 @@ EXPORTED = (
     "swattn_shared_scores", "swattn_topk_blocks", "swattn_select_blocks", "swattn_sparse_fwd",
     "swattn_sparse_workspace_bytes",
     "swattn_dense_fwd", "swattn_attend", "swattn_select_blocks_rows", "swattn_sparse_fwd_rows",
-    "swattn_attend_rows", "swattn_attend_prepare", "swattn_kcache_append", "swattn_decode_step",
+    "swattn_attend_rows", "swattn_attend_prepare", "swattn_workspace_ckeys", "swattn_kcache_append", "swattn_decode_step",
     "swattn_decode_workspace_bytes",
 )
 

@@ -322,6 +322,8 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;
   if ((rc = check_rows(cfg, n, r0, r1))) return rc;
+  const bool prepared = (mode & SWATTN_SELECT_PREPARED) != 0;
+  mode &= ~SWATTN_SELECT_PREPARED;
   if (mode < 0 || mode > 2) {
     set_error("unknown selection mode %d", mode);
     return SWATTN_EINVAL;
@@ -341,7 +343,7 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
   int32_t *rows = reinterpret_cast<int32_t *>(ws + L.off_rows);
   // the compressed keys of the whole sequence are built by the call that
   // covers row 0 and stay in the workspace for the later row ranges
-  if (r0 == 0 && (rc = launch_compress(cfg, K, n, kc1, kc2, st))) return rc;
+  if (r0 == 0 && !prepared && (rc = launch_compress(cfg, K, n, kc1, kc2, st))) return rc;
   if (cfg->k_top == 0 || L.n_cols <= cfg->N_init) {
     if (cfg->k_top > 0 &&
         (rc = memset_rows(topk, n, cfg->h_kv, r0, r1, (size_t)cfg->k_top * 4, 0xff, st)))
@@ -525,6 +527,20 @@ int32_t swattn_attend_prepare(const swattn_config *cfg, const void *K, int64_t n
   }
   char *ws = static_cast<char *>(workspace);
   return launch_compress(cfg, K, n, ws + L.off_kc1, ws + L.off_kc2, static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_workspace_ckeys(const swattn_config *cfg, int64_t n, void *workspace, void **kc1,
+                               void **kc2) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1 || workspace == nullptr || kc1 == nullptr || kc2 == nullptr) {
+    set_error("swattn_workspace_ckeys: need n >= 1 and non-NULL pointers");
+    return SWATTN_EINVAL;
+  }
+  const SelectLayout L = select_layout(cfg, n);
+  *kc1 = static_cast<char *>(workspace) + L.off_kc1;
+  *kc2 = static_cast<char *>(workspace) + L.off_kc2;
+  return SWATTN_OK;
 }
 
 int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *K, const void *V,

@@ -356,3 +356,36 @@ def test_context_parallel_ranks_reassemble_whole():
         torch.cuda.synchronize()
         assert covered[0][0] == 0 and covered[-1][1] == Qd.shape[0]
         assert torch.equal(O, whole.output) and torch.equal(lse, whole.lse), world
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,world", [("paper_n16384_s2", 4), ("paper_n10000_s1", 3)])
+def test_context_parallel_sharded_inputs(name, world):
+    """Sequence-sharded context parallelism (parallel.context_parallel_attend_
+    sharded) with its collectives replaced by in-process gathers: per-rank K1
+    on the shard + halo reassembles the global compressed keys bit for bit,
+    and each rank's rows computed from separately allocated Q / O shards
+    (virtual row-0 base pointers) equal the whole-sequence attend."""
+    from paper_2509_24663_b200.parallel import (cp_attend_rows, cp_halo_rows, cp_install_ckeys,
+                                                cp_local_ckeys, shard_rows)
+    from paper_2509_24663_b200.selection import Workspace
+    rec, prof, cfg, _, (Qd, Kd, Vd) = _load(name)
+    n = Qd.shape[0]
+    whole, _ = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    k1, k2 = mean_pool_keys(Kd, cfg.l_C1, cfg.s_C1), mean_pool_keys(Kd, cfg.l_C2, cfg.s_C2)
+    bounds = shard_rows(n, world)
+    H = cp_halo_rows(cfg)
+    parts = [cp_local_ckeys(Kd[a: min(n, b + H)].clone(), cfg, n, a, b) for a, b in bounds]
+    kc1 = torch.cat([p[0] for p in parts])
+    kc2 = torch.cat([p[1] for p in parts])
+    assert torch.equal(kc1, k1.keys) and torch.equal(kc2, k2.keys)
+    L = _lib.lib()
+    ws = Workspace.get(L.swattn_workspace_bytes(_lib.c_config(cfg), n), Qd.device)
+    cp_install_ckeys(ws, cfg, n, kc1, kc2)
+    for a, b in bounds:
+        Q_sh = Qd[a:b].clone()
+        O_sh = torch.full((b - a, 32, 128), float("nan"), dtype=torch.bfloat16, device="cuda")
+        l_sh = torch.full((b - a, 32), float("nan"), dtype=torch.float32, device="cuda")
+        cp_attend_rows(Q_sh, Kd, Vd, cfg, n, a, b, ws, O_sh, l_sh)
+        torch.cuda.synchronize()
+        assert torch.equal(O_sh, whole.output[a:b]) and torch.equal(l_sh, whole.lse[a:b]), (a, b)
