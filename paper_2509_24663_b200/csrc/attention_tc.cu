@@ -239,28 +239,31 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         x[c] = v;
         mx = fmaxf(mx, v);
       }
-      if (mx > m + kRescaleThresh || m == -INFINITY) {
-        const float m_new = fmaxf(mx, m);
-        if (m != -INFINITY && i > 0) {
-          // S_i completing implies PV_{i-2} completed (issue order S_i after
-          // PV_{i-2}), so o_done has 0 or 1 pending phase: the parity wait
-          // for completion #i (PV_{i-1}) is unambiguous.
-          const float alpha = fast_exp2(m - m_new);
-          tc::mbar_wait(&s.o_done, (i - 1) & 1);
-          tc::tc_fence_after();
+      // Lazy rescale.  tcgen05.ld / st are warp-collective (.sync.aligned), so
+      // the O read-modify-write runs for the whole warp whenever any of its
+      // rows needs it; rows that do not scale by 1.
+      const bool want = mx > m + kRescaleThresh || m == -INFINITY;
+      const float m_new = want ? fmaxf(mx, m) : m;
+      const bool resc = want && m != -INFINITY && i > 0;
+      if (__any_sync(0xffffffffu, resc)) {
+        // S_i completing implies PV_{i-2} completed (issue order S_i after
+        // PV_{i-2}), so o_done has 0 or 1 pending phase: the parity wait
+        // for completion #i (PV_{i-1}) is unambiguous.
+        const float alpha = resc ? fast_exp2(m - m_new) : 1.f;
+        tc::mbar_wait(&s.o_done, (i - 1) & 1);
+        tc::tc_fence_after();
 #pragma unroll
-          for (int c0 = 0; c0 < kD; c0 += 32) {
-            uint32_t o[32];
-            tc::tmem_ld32(tmem_o + lane_off + c0, o);
-            tc::tmem_ld_wait();
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          tc::tmem_ld32(tmem_o + lane_off + c0, o);
+          tc::tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tc::tmem_st32(tmem_o + lane_off + c0, o);
-          }
-          l *= alpha;
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tc::tmem_st32(tmem_o + lane_off + c0, o);
         }
-        m = m_new;
+        l *= alpha;
       }
+      m = m_new;
       uint32_t pk[kBlk / 2];
       float rs = 0.f;
 #pragma unroll

@@ -86,18 +86,22 @@ __device__ __forceinline__ void pass1_keys(const RerankArgs &a, const RowInfo &r
   vis = use_c2 ? vis2 : vis1;
 }
 
-__device__ void load_q(const RerankArgs &a, const RowInfo &r, double (*q_s)[kD]) {
+// q_s is [d][head]: the 16 heads of one d are 128 contiguous bytes, so a
+// thread's 4-head register tile is two 16-byte broadcasts and the 16 lanes
+// of a member-scoring half-warp read 16 different heads conflict-free.
+__device__ void load_q(const RerankArgs &a, const RowInfo &r, double (*q_s)[kG]) {
   for (int t = threadIdx.x; t < kG * kD; t += kThreads) {
     const int h = t / kD, d = t % kD;
-    q_s[h][d] = (double)bf2f(a.Q[(r.qrow * a.h_q + r.g * kG + h) * kD + d]);
+    q_s[d][h] = (double)bf2f(a.Q[(r.qrow * a.h_q + r.g * kG + h) * kD + d]);
   }
 }
 
 // float64 (max, sum) of the 16 heads over normaliser columns [c_lo, c_hi),
-// 128-column chunks staged as doubles [d][c]; thread = 4 heads x 2 columns
-// register tile (8 DFMA per 3 shared loads).  Result in mh[h], lh[h].
+// 128-column chunks staged as bf16 [d][c] (32 KB, so two CTAs fit an SM);
+// thread = 4 heads x 2 columns register tile (8 DFMA per 3 shared loads).
+// Result in mh[h], lh[h].
 __device__ void pass1_range(const RerankArgs &a, const __nv_bfloat16 *kc, int g, int64_t c_lo,
-                            int64_t c_hi, const double (*q_s)[kD], double *kc_s,
+                            int64_t c_hi, const double (*q_s)[kG], __nv_bfloat16 *kc_s,
                             double (*wm)[4], double (*wl)[4], double *mh, double *lh) {
   const int hg = threadIdx.x / 64, cg = threadIdx.x % 64;
   double mloc[4], lloc[4];
@@ -111,7 +115,7 @@ __device__ void pass1_range(const RerankArgs &a, const __nv_bfloat16 *kc, int g,
       if (c0 + c < c_hi) raw = __ldg(reinterpret_cast<const uint4 *>(kc + ((c0 + c) * a.h_kv + g) * kD + d0));
       const __nv_bfloat16 *kv = reinterpret_cast<const __nv_bfloat16 *>(&raw);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) kc_s[(d0 + e) * kChunk + c] = (double)bf2f(kv[e]);
+      for (int e = 0; e < 8; ++e) kc_s[(d0 + e) * kChunk + c] = kv[e];
     }
     __syncthreads();
     double acc[4][2];
@@ -119,12 +123,15 @@ __device__ void pass1_range(const RerankArgs &a, const __nv_bfloat16 *kc, int g,
     for (int e = 0; e < 4; ++e) acc[e][0] = acc[e][1] = 0.0;
 #pragma unroll 4
     for (int d = 0; d < kD; ++d) {
-      const double2 kk = *reinterpret_cast<const double2 *>(&kc_s[d * kChunk + 2 * cg]);
+      const uint32_t kk2 = *reinterpret_cast<const uint32_t *>(&kc_s[d * kChunk + 2 * cg]);
+      const double kx = (double)__uint_as_float(kk2 << 16), ky = (double)__uint_as_float(kk2 & 0xffff0000u);
+      const double2 q01 = *reinterpret_cast<const double2 *>(&q_s[d][4 * hg]);
+      const double2 q23 = *reinterpret_cast<const double2 *>(&q_s[d][4 * hg + 2]);
+      const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const double qv = q_s[4 * hg + e][d];
-        acc[e][0] = fma(qv, kk.x, acc[e][0]);
-        acc[e][1] = fma(qv, kk.y, acc[e][1]);
+        acc[e][0] = fma(qv[e], kx, acc[e][0]);
+        acc[e][1] = fma(qv[e], ky, acc[e][1]);
       }
     }
 #pragma unroll
@@ -164,11 +171,11 @@ __device__ void pass1_range(const RerankArgs &a, const __nv_bfloat16 *kc, int g,
 }
 
 // pass-1 partials for the row-split path: work item = (flagged row, column slice)
-__global__ void __launch_bounds__(kThreads) rerank_p1_kernel(RerankArgs a) {
-  __shared__ double q_s[kG][kD];
+__global__ void __launch_bounds__(kThreads, 2) rerank_p1_kernel(RerankArgs a) {
+  __shared__ __align__(16) double q_s[kD][kG];
   __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
   __shared__ double mh[kG], lh[kG];
-  extern __shared__ double kc_s[];  // [kD][kChunk]
+  extern __shared__ __nv_bfloat16 kc_s[];  // [kD][kChunk]
   const int total = min(*a.count, a.cap);
   if (total > kSplitRows || a.partials == nullptr) return;
   for (int w = blockIdx.x; w < total * kP1Split; w += gridDim.x) {
@@ -208,11 +215,11 @@ __device__ double block_reduce_sum(double v, double *red) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
-  __shared__ double q_s[kG][kD];
+__global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
+  __shared__ __align__(16) double q_s[kD][kG];
   __shared__ double lse_s[kG];
   __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
-  extern __shared__ double kc_s[];  // [kD][kChunk]
+  extern __shared__ __nv_bfloat16 kc_s[];  // [kD][kChunk]
   __shared__ double red[kThreads / 32];
   __shared__ int members[kMaxCluster];
   __shared__ double mscore[kMaxCluster];
@@ -286,26 +293,43 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     __syncthreads();
     const int nm = min(n_members, kMaxCluster);
 
-    // ---- float64 max-pooled scores of the cluster members
+    // ---- float64 max-pooled scores of the cluster members: warp = member,
+    // lane = (head lane & 15, window columns lane >> 4, +2, +4); each lane
+    // runs its dot products serially over d, heads are summed by shuffles
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hh = lane & 15, c_half = lane >> 4;
     for (int mi = warp; mi < nm; mi += kThreads / 32) {
       const int j = members[mi];
-      double best = -INFINITY;
-      for (int e = 0; e < a.pl; ++e) {
+      double val[3];
+      bool inwin[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int e = c_half + 2 * q;
         const int64_t c = (int64_t)j * a.ps + e;
-        if (c >= m1) break;
-        double sh = 0.0;
-        if (c < vis1) {
-          const __nv_bfloat16 *kr = kc1 + (c * a.h_kv + g) * kD;
-          for (int h = 0; h < kG; ++h) {
-            double dot = 0.0;
-            for (int d = lane; d < kD; d += 32) dot = fma(q_s[h][d], (double)bf2f(kr[d]), dot);
-            for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-            sh += exp(dot * a.scale - lse_s[h]);
+        inwin[q] = e < a.pl && c < m1;   // window columns past m1 do not exist
+        double dot = 0.0;
+        if (inwin[q] && c < vis1) {
+          const uint32_t *kr = reinterpret_cast<const uint32_t *>(kc1 + (c * a.h_kv + g) * kD);
+#pragma unroll 8
+          for (int d2 = 0; d2 < kD / 2; ++d2) {
+            const uint32_t kk2 = __ldg(kr + d2);
+            dot = fma(q_s[2 * d2][hh], (double)__uint_as_float(kk2 << 16), dot);
+            dot = fma(q_s[2 * d2 + 1][hh], (double)__uint_as_float(kk2 & 0xffff0000u), dot);
           }
+          val[q] = exp(dot * a.scale - lse_s[hh]);
+        } else {
+          val[q] = 0.0;  // not visible: contributes nothing (selection.py:212-222)
         }
-        best = fmax(best, sh);
       }
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) val[q] += __shfl_xor_sync(0xffffffffu, val[q], o);
+      double best = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (inwin[q]) best = fmax(best, val[q]);
+      best = fmax(best, __shfl_xor_sync(0xffffffffu, best, 16));
       if (lane == 0) mscore[mi] = best;
     }
     __syncthreads();
@@ -315,7 +339,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
     // blocks + chosen members) in the now idle staging buffer, emitted in
     // ascending order by a block-wide scan of per-thread word counts.
     uint32_t *bits = reinterpret_cast<uint32_t *>(kc_s);
-    int *wsum = reinterpret_cast<int *>(kc_s) + (kChunk * kD * 2 - kThreads);  // tail of kc_s
+    int *wsum = reinterpret_cast<int *>(kc_s) + (kChunk * kD / 2 - kThreads);  // tail of kc_s
     const int nwords = (ncand + 31) >> 5;
     for (int w = threadIdx.x; w < nwords; w += kThreads) bits[w] = 0u;
     __syncthreads();
@@ -369,7 +393,7 @@ __global__ void __launch_bounds__(kThreads) rerank_kernel(RerankArgs a) {
 }
 
 int32_t run_rerank(const RerankArgs &a, int num_sms, cudaStream_t stream) {
-  const size_t smem = (size_t)kD * kChunk * sizeof(double);
+  const size_t smem = (size_t)kD * kChunk * sizeof(__nv_bfloat16);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

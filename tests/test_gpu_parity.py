@@ -389,3 +389,57 @@ def test_context_parallel_sharded_inputs(name, world):
         cp_attend_rows(Q_sh, Kd, Vd, cfg, n, a, b, ws, O_sh, l_sh)
         torch.cuda.synchronize()
         assert torch.equal(O_sh, whole.output[a:b]) and torch.equal(l_sh, whole.lse[a:b]), (a, b)
+
+
+@pytest.mark.gpu
+def test_selection_all_tied_scores():
+    """Q = 0 makes every candidate block of a row score exactly the same
+    (shared = G / visible in float64 and float32 alike), so the stable
+    argsort (selection.py:125) keeps the k lowest block ids.  Exercises K3's
+    massive-tie path (the register path's survivor overflow) and the float64
+    re-rank of every flagged row; checked in closed form for all rows and
+    against the oracle on sampled rows."""
+    n = 8192
+    cfg = AttentionConfig()
+    prof = O.Profile()
+    _, K, _ = O.draw_qkv(n, 32, 2, 128, 11)
+    Q = np.zeros((n, 32, 128), dtype=K.dtype)
+    sel = select_blocks(_dev(Q), _dev(K), cfg, mode="approx")
+    got = sel.topk.cpu().numpy().astype(np.int64)
+    cnt = sel.topk_cnt.cpu().numpy()
+    for i in range(0, n, 7):
+        k = int(cnt[0, i])
+        for g in range(2):
+            assert np.array_equal(got[g, i, :k], np.arange(cfg.N_init, cfg.N_init + k)), (g, i)
+    rows = np.array([4100, 5000, 8191])
+    want, _, _ = O.select(Q, K, prof, mode="approx", rows=rows)
+    assert np.array_equal(got[:, rows, :cfg.k_top], want.astype(np.int64)[:, :, :cfg.k_top])
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("scale", [3.0, 8.0])
+def test_large_logits_dense_and_part_a(scale):
+    """Logits spread wide enough that the running row max of the FA tile
+    (K5 and part A) grows by more than its lazy-rescale threshold at
+    different blocks for different rows of one warp: the O rescale must
+    stay warp-collective (regression: a divergent tcgen05.ld hung the GPU on
+    projected MiniCPM activations) and match the float64 oracle."""
+    n = 8192
+    cfg = AttentionConfig()
+    prof = O.Profile()
+    Q, K, V = O.draw_qkv(n, 32, 2, 128, 5)
+    Qs = (Q.astype(np.float32) * scale).astype(Q.dtype)
+    Qd, Kd, Vd = _dev(Qs), _dev(K), _dev(V)
+    rows = np.array([0, 1, 63, 64, 700, 4095, 4096, 6000, 8191])
+    dense = tiled_gqa_forward(Qd, Kd, Vd, cfg)
+    torch.cuda.synchronize()
+    want_o, want_l = O.dense_attention(Qs, K, V, prof, rows=rows)
+    r = torch.as_tensor(rows, device="cuda")
+    _tol(dense.output[r], want_o, dense.lse[r], want_l)
+    res, mode = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    torch.cuda.synchronize()
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    topk = sel.topk.cpu().numpy().astype(np.int64)
+    want_o, want_l = O.sparse_attention(Qs, K, V, topk, prof, rows=rows)
+    _tol(res.output[r], want_o, res.lse[r], want_l)

@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 from paper_2509_24663_b200.core import AttentionConfig  # noqa: E402
 from paper_2509_24663_b200.switch import attend  # noqa: E402
 
-D, LAYERS, HQ, HKV, DH, FF = 4096, 32, 32, 2, 128, 16384
+D, HQ, HKV, DH, FF = 4096, 32, 2, 128, 16384
+LAYERS = int(os.environ.get("MINICPM_LAYERS", 32))
 SCALE_DEPTH = 1.4
 ROWS = 16384  # row chunk of the FFN (bounds the 2 x 16384-wide intermediate)
 
@@ -130,15 +131,22 @@ def run(n, layers, cfg, attn_fn, reps=2):
 
 
 def main():
+    if os.environ.get("MINICPM_WATCHDOG"):  # debugging: dump the stacks of a hung run
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["MINICPM_WATCHDOG"]), exit=True)
     sizes = [int(x) for x in sys.argv[1:]] or [4096, 32768, 131072]
     dev = torch.device("cuda")
     gen = torch.Generator(device=dev).manual_seed(0)
+    print("building weights", file=sys.stderr, flush=True)
     layers = [Layer(dev, gen) for _ in range(LAYERS)]
     cfg = AttentionConfig()
     lin_flops_per_tok = 2 * LAYERS * (D * (HQ + 2 * HKV) * DH + HQ * DH * D + D * 2 * FF + FF * D)
+    print(f"weights ready ({LAYERS} layers)", file=sys.stderr, flush=True)
     for n in sizes:
         ours = run(n, layers, cfg, attn_ours)
+        print(f"n={n} ours {ours[0]:.1f} ms", file=sys.stderr, flush=True)
         dense = run(n, layers, cfg, attn_cudnn)
+        print(f"n={n} cudnn {dense[0]:.1f} ms", file=sys.stderr, flush=True)
         line = {"n": n, "layers": LAYERS, "weights": "random N(0,0.02) bf16", "attention_mode": ours[2],
                 "ms": ours[0], "tokens_per_s": n / (ours[0] / 1e3), "attention_ms": ours[1],
                 "attention_share": ours[1] / ours[0], "finite": ours[3],
