@@ -227,18 +227,29 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       tc::tmem_ld32(tmem + lane_off + (i & 1) * kBlk, ra);
       tc::tmem_ld32(tmem + lane_off + (i & 1) * kBlk + 32, rb);
       tc::tmem_ld_wait();
+      // raw logits; the scale is folded into the exp argument (one FFMA per
+      // element) and masking runs only on the diagonal / padded block
       float x[kBlk];
       const int64_t key0 = (int64_t)jb * kBlk;
       const bool diag = (p.mode != 1) && (key0 + kBlk - 1 > tok);
-      float mx = -INFINITY;
+      const bool pad = (p.mode == 1) && (key0 + kBlk > p.n);
 #pragma unroll
-      for (int c = 0; c < kBlk; ++c) {
-        float v = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]) * p.scale_log2;
-        if (diag && key0 + c > tok) v = -INFINITY;
-        if (p.mode == 1 && key0 + c >= p.n) v = -INFINITY;
-        x[c] = v;
-        mx = fmaxf(mx, v);
+      for (int c = 0; c < kBlk; ++c) x[c] = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
+      if (diag || pad) {
+        const int64_t lim = diag ? tok - key0 : p.n - 1 - key0;  // last visible column
+#pragma unroll
+        for (int c = 0; c < kBlk; ++c)
+          if (c > lim) x[c] = -INFINITY;
       }
+      float mx0 = x[0], mx1 = x[1], mx2 = x[2], mx3 = x[3];
+#pragma unroll
+      for (int c = 4; c < kBlk; c += 4) {
+        mx0 = fmaxf(mx0, x[c]);
+        mx1 = fmaxf(mx1, x[c + 1]);
+        mx2 = fmaxf(mx2, x[c + 2]);
+        mx3 = fmaxf(mx3, x[c + 3]);
+      }
+      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
       // Lazy rescale.  tcgen05.ld / st are warp-collective (.sync.aligned), so
       // the O read-modify-write runs for the whole warp whenever any of its
       // rows needs it; rows that do not scale by 1.
@@ -268,8 +279,8 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < kBlk; c += 2) {
-        const float p0 = fast_exp2(x[c] - m);
-        const float p1 = fast_exp2(x[c + 1] - m);
+        const float p0 = fast_exp2(fmaf(x[c], p.scale_log2, -m));
+        const float p1 = fast_exp2(fmaf(x[c + 1], p.scale_log2, -m));
         rs += p0 + p1;
         pk[c / 2] = tc::pack_bf16(p0, p1);
       }
