@@ -315,10 +315,16 @@ static int32_t memset_rows(void *base, int64_t n, int h_kv, int64_t r0, int64_t 
   return SWATTN_OK;
 }
 
+// Work forked onto a side stream once K2 is queued (attend: part A of K4,
+// which then shares the SMs with the latency-bound K3 / re-rank kernels).
+struct AfterScores {
+  virtual int32_t run(cudaStream_t st) = 0;
+};
+
 static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *K, int64_t n,
                            int64_t r0, int64_t r1, int32_t mode, int32_t *topk, int32_t *topk_cnt,
                            int32_t *n_reranked, void *workspace, size_t workspace_bytes,
-                           cudaStream_t st) {
+                           cudaStream_t st, AfterScores *after_scores = nullptr) {
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;
   if ((rc = check_rows(cfg, n, r0, r1))) return rc;
@@ -373,6 +379,7 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
   else
     rc = launch_scores_simt(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
   if (rc) return rc;
+  if (after_scores != nullptr && (rc = after_scores->run(st))) return rc;
   if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset(count)"))) return rc;
   const int32_t cap = (int32_t)((int64_t)cfg->h_kv * n);
   if ((rc = launch_topk(cfg, scmp, L.ld, n, r0, r1, topk, topk_cnt, count, rows, cap, flags,
@@ -387,10 +394,83 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
   return SWATTN_OK;
 }
 
+// Part A of K4 (init + local blocks, shared by a query block's 64 tokens)
+// needs no selection, so attend forks it onto a side stream once K2 is
+// queued: it fills the SMs the latency-bound K3 / re-rank kernels leave idle
+// and joins before part B.  (Forking before K2 gained nothing: K2 is MUFU-
+// bound and so is the FA tile's softmax.)  The side stream and events are
+// per host thread and device (created once).
+struct SideStream {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static int32_t side_stream(SideStream *&out) {
+  thread_local SideStream ss[16];
+  int dev = 0;
+  int32_t rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc) return rc;
+  SideStream &x = ss[dev & 15];
+  if (x.device != dev) {
+    if ((rc = cuda_check(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking), "side stream")) ||
+        (rc = cuda_check(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming), "side event")) ||
+        (rc = cuda_check(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming), "side event")))
+      return rc;
+    x.device = dev;
+  }
+  out = &x;
+  return SWATTN_OK;
+}
+
+static int32_t sparse_ws_ptrs(const swattn_config *cfg, int64_t n, void *workspace, float *&m_a,
+                              float *&l_a, int32_t *&slow_count, int32_t *&slow_list) {
+  char *ws = static_cast<char *>(workspace);
+  m_a = reinterpret_cast<float *>(ws);
+  l_a = reinterpret_cast<float *>(ws + align_up((size_t)n * cfg->h_q * 4));
+  slow_count = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4));
+  slow_list = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4) + align_up(16));
+  return SWATTN_OK;
+}
+
+static bool overlap_ok(const swattn_config *cfg) {
+  return use_tc_attention() && swattn_profile_supported(cfg) && cfg->h_q == kG * cfg->h_kv &&
+         cfg->d_h == kD;
+}
+
+// fork part A of rows [r0, r1) onto the side stream (after everything queued on st)
+static int32_t part_a_fork(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                           int64_t n, int64_t r0, int64_t r1, void *O, float *lse, void *sparse_ws,
+                           cudaStream_t st, SideStream *&side) {
+  int32_t rc = side_stream(side);
+  if (rc) return rc;
+  float *m_a, *l_a;
+  int32_t *slow_count, *slow_list;
+  sparse_ws_ptrs(cfg, n, sparse_ws, m_a, l_a, slow_count, slow_list);
+  if ((rc = cuda_check(cudaEventRecord(side->fork, st), "event record")) ||
+      (rc = cuda_check(cudaStreamWaitEvent(side->stream, side->fork, 0), "stream wait")))
+    return rc;
+  if ((rc = launch_sparse_part_a(cfg, Q, K, V, n, r0, r1, O, lse, m_a, l_a, side->stream))) return rc;
+  return cuda_check(cudaEventRecord(side->join, side->stream), "event record");
+}
+
+static int32_t sparse_rows_impl(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                                int64_t n, int64_t r0, int64_t r1, const int32_t *topk,
+                                const int32_t *topk_cnt, void *O, float *lse, void *workspace,
+                                size_t workspace_bytes, cudaStream_t st, bool part_a_done);
+
 static int32_t sparse_rows(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                            int64_t n, int64_t r0, int64_t r1, const int32_t *topk,
                            const int32_t *topk_cnt, void *O, float *lse, void *workspace,
                            size_t workspace_bytes, cudaStream_t st) {
+  return sparse_rows_impl(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, O, lse, workspace,
+                          workspace_bytes, st, false);
+}
+
+static int32_t sparse_rows_impl(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                                int64_t n, int64_t r0, int64_t r1, const int32_t *topk,
+                                const int32_t *topk_cnt, void *O, float *lse, void *workspace,
+                                size_t workspace_bytes, cudaStream_t st, bool part_a_done) {
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;
   if ((rc = check_rows(cfg, n, r0, r1))) return rc;
@@ -410,7 +490,8 @@ static int32_t sparse_rows(const swattn_config *cfg, const void *Q, const void *
     int32_t *slow_count = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4));
     int32_t *slow_list = reinterpret_cast<int32_t *>(ws + 2 * align_up((size_t)n * cfg->h_q * 4) +
                                                      align_up(16));
-    if ((rc = launch_sparse_part_a(cfg, Q, K, V, n, r0, r1, O, lse, m_a, l_a, st))) return rc;
+    if (!part_a_done && (rc = launch_sparse_part_a(cfg, Q, K, V, n, r0, r1, O, lse, m_a, l_a, st)))
+      return rc;
     if ((rc = cuda_check(cudaMemsetAsync(slow_count, 0, 4, st), "memset(slow)"))) return rc;
     if ((rc = launch_sparse_part_b(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, m_a, l_a, O, lse,
                                    slow_count, slow_list, num_sms(), st)))
@@ -423,6 +504,44 @@ static int32_t sparse_rows(const swattn_config *cfg, const void *Q, const void *
     return SWATTN_EUNSUPPORTED;
   }
   return launch_attention_simt(cfg, Q, K, V, n, topk, topk_cnt, 1, 1, O, lse, nullptr, st);
+}
+
+// select rows [r0, r1) on st, with part A of the same rows running
+// concurrently on the side stream, then part B on st.
+static int32_t select_and_sparse(const swattn_config *cfg, const void *Q, const void *K,
+                                 const void *V, int64_t n, int64_t r0, int64_t r1, int32_t select_mode,
+                                 int32_t *topk, int32_t *cnt, void *O, float *lse, void *sel_ws,
+                                 size_t sel_bytes, void *sparse_ws, size_t sparse_bytes,
+                                 cudaStream_t st) {
+  int32_t rc = check_rows(cfg, n, r0, r1);
+  if (rc) return rc;
+  const bool overlap = overlap_ok(cfg) && sparse_ws != nullptr &&
+                       sparse_bytes >= swattn_sparse_workspace_bytes(cfg, n);
+  struct ForkPartA : AfterScores {
+    const swattn_config *cfg;
+    const void *Q, *K, *V;
+    int64_t n, r0, r1;
+    void *O;
+    float *lse;
+    void *sparse_ws;
+    SideStream *side = nullptr;
+    int32_t run(cudaStream_t s) override {
+      return part_a_fork(cfg, Q, K, V, n, r0, r1, O, lse, sparse_ws, s, side);
+    }
+  } fork;
+  fork.cfg = cfg; fork.Q = Q; fork.K = K; fork.V = V; fork.n = n; fork.r0 = r0; fork.r1 = r1;
+  fork.O = O; fork.lse = lse; fork.sparse_ws = sparse_ws;
+  rc = select_rows(cfg, Q, K, n, r0, r1, select_mode, topk, cnt, nullptr, sel_ws, sel_bytes, st,
+                   overlap ? &fork : nullptr);
+  const bool forked = fork.side != nullptr;
+  if (forked) {
+    // join even on failure so the side stream never outlives the call's buffers
+    const int32_t rj = cuda_check(cudaStreamWaitEvent(st, fork.side->join, 0), "stream wait");
+    if (!rc) rc = rj;
+  }
+  if (rc) return rc;
+  return sparse_rows_impl(cfg, Q, K, V, n, r0, r1, topk, cnt, O, lse, sparse_ws, sparse_bytes, st,
+                          forked);
 }
 
 }  // namespace swattn
@@ -503,13 +622,11 @@ int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, co
   int32_t *topk = reinterpret_cast<int32_t *>(ws + align_up(L.total));
   int32_t *cnt = reinterpret_cast<int32_t *>(ws + align_up(L.total) +
                                              align_up((size_t)cfg->h_kv * n * cfg->k_top * 4));
-  if ((rc = swattn_select_blocks(cfg, Q, K, n, select_mode, topk, cnt, nullptr, workspace, L.total,
-                                 stream)))
-    return rc;
   char *sws = ws + align_up(L.total) + align_up((size_t)cfg->h_kv * n * cfg->k_top * 4) +
               align_up((size_t)cfg->h_kv * n * 4);
-  return swattn_sparse_fwd(cfg, Q, K, V, n, topk, cnt, O, lse, sws,
-                           swattn_sparse_workspace_bytes(cfg, n), stream);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return select_and_sparse(cfg, Q, K, V, n, 0, n, select_mode, topk, cnt, O, lse, workspace, L.total,
+                           sws, swattn_sparse_workspace_bytes(cfg, n), st);
 }
 
 int32_t swattn_attend_prepare(const swattn_config *cfg, const void *K, int64_t n, void *workspace,
@@ -559,13 +676,10 @@ int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *
   int32_t *cnt = reinterpret_cast<int32_t *>(ws + align_up(L.total) +
                                              align_up((size_t)cfg->h_kv * n * cfg->k_top * 4));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((rc = select_rows(cfg, Q, K, n, r0, r1, select_mode, topk, cnt, nullptr, workspace, L.total,
-                        st)))
-    return rc;
   char *sws = ws + align_up(L.total) + align_up((size_t)cfg->h_kv * n * cfg->k_top * 4) +
               align_up((size_t)cfg->h_kv * n * 4);
-  return sparse_rows(cfg, Q, K, V, n, r0, r1, topk, cnt, O, lse, sws,
-                     swattn_sparse_workspace_bytes(cfg, n), st);
+  return select_and_sparse(cfg, Q, K, V, n, r0, r1, select_mode, topk, cnt, O, lse, workspace,
+                           L.total, sws, swattn_sparse_workspace_bytes(cfg, n), st);
 }
 
 }  // extern "C"

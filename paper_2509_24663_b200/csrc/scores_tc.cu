@@ -202,14 +202,26 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&s.tempty[tb]);
+      // raw logits; the scale is folded into the exp FFMA and the visibility
+      // mask only runs on the chunk that crosses my_vis
       float x[64];
-      float cm = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 64; ++e) {
-        const uint32_t uu = e < 32 ? va[e] : vb[e - 32];
-        x[e] = (c0 + e < my_vis) ? __uint_as_float(uu) * p.scale_log2 : -INFINITY;
-        cm = fmaxf(cm, x[e]);
+      for (int e = 0; e < 64; ++e) x[e] = __uint_as_float(e < 32 ? va[e] : vb[e - 32]);
+      if (c0 + 64 > my_vis) {
+        const int64_t lim = my_vis - c0;  // columns e >= lim are not visible
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          if (e >= lim) x[e] = -INFINITY;
       }
+      float cm0 = x[0], cm1 = x[1], cm2 = x[2], cm3 = x[3];
+#pragma unroll
+      for (int e = 4; e < 64; e += 4) {
+        cm0 = fmaxf(cm0, x[e]);
+        cm1 = fmaxf(cm1, x[e + 1]);
+        cm2 = fmaxf(cm2, x[e + 2]);
+        cm3 = fmaxf(cm3, x[e + 3]);
+      }
+      const float cm = fmaxf(fmaxf(cm0, cm1), fmaxf(cm2, cm3)) * p.scale_log2;
       if (cm > m) {
         l *= fast_exp2(m - cm);
         m = cm;
@@ -217,10 +229,10 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
       for (int e = 0; e < 64; e += 4) {
-        a0 += fast_exp2(x[e] - m);
-        a1 += fast_exp2(x[e + 1] - m);
-        a2 += fast_exp2(x[e + 2] - m);
-        a3 += fast_exp2(x[e + 3] - m);
+        a0 += fast_exp2(fmaf(x[e], p.scale_log2, -m));
+        a1 += fast_exp2(fmaf(x[e + 1], p.scale_log2, -m));
+        a2 += fast_exp2(fmaf(x[e + 2], p.scale_log2, -m));
+        a3 += fast_exp2(fmaf(x[e + 3], p.scale_log2, -m));
       }
       if (m != -INFINITY) l += (a0 + a1) + (a2 + a3);
     }

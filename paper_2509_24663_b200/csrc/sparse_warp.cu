@@ -24,11 +24,14 @@
 //
 // Data movement: each warp streams its token's selected blocks as 16-key
 // stages (K and V, 4 KB each, one 4-D TMA box per tensor, 128-byte swizzle)
-// through its own 2-stage mbarrier ring (8 warps x 2 stages measured best:
-// tools/probe_variants.sh sweep, 37.5 ms vs 41.5 ms for 3 stages at 128K); lane 0 is the warp's TMA issuer, so
-// a CTA has 8 independent issuers (a single issuing thread caps near
-// 36 GB/s, tools/gather_bench.cu).  The ring runs across token boundaries and
-// the next token's Q is fetched while the current one computes.
+// through its own 2-stage mbarrier ring; lane 0 is the warp's TMA issuer, so
+// a CTA has 12 independent issuers (a single issuing thread caps near
+// 36 GB/s, tools/gather_bench.cu).  The ring runs across token boundaries.
+// Q fragments are loaded straight from global memory (L2) into registers,
+// which frees the Q smem slot: 12 warps x 2 stages (192 KB, 168 registers)
+// measured best (tools/probe_partb.sh, profiles/r01c_partb_probe.txt:
+// w12 34.3 ms, w10 37.4, w8 35.6, w8 + TMA'd Q 37.7, w8 x 3 stages 40.2,
+// w6 x 4 stages 46.0 at 128K) -- deeper rings lose, more warps win.
 // Roofline: the L2->SMEM gather of 2 x cnt x 16 KB per (token, group).
 #include <string.h>
 
@@ -42,10 +45,13 @@ namespace {
 
 // geometry (overridable for tuning sweeps: tools/build_variants.sh EXTRA=-D...)
 #ifndef SWATTN_PW_WARPS
-#define SWATTN_PW_WARPS 8
+#define SWATTN_PW_WARPS 12
 #endif
 #ifndef SWATTN_PW_STAGES
 #define SWATTN_PW_STAGES 2
+#endif
+#ifndef SWATTN_PW_QGLOBAL
+#define SWATTN_PW_QGLOBAL 1  // Q fragments straight from global memory (0: TMA into a Q smem slot)
 #endif
 #ifndef SWATTN_PW_IPW
 #define SWATTN_PW_IPW 0  // items (tokens) per warp; 0 = persistent grid of num_sms CTAs
@@ -73,6 +79,7 @@ struct PwParams {
   int64_t n_items;     // h_kv * (tok1 - tok0)
   const int32_t *topk, *topk_cnt;
   const float *m_a, *l_a;  // part A row statistics [n][h_q] (log2 max, sum)
+  const __nv_bfloat16 *Q;  // [n][h_q][d] (QGLOBAL variant)
   __nv_bfloat16 *O;        // in: O_A (normalised), out: final
   float *lse;
   float scale_log2;
@@ -82,7 +89,9 @@ struct PwParams {
 struct __align__(1024) WarpSmem {
   uint8_t k[kStages][kTileBytes];
   uint8_t v[kStages][kTileBytes];
+#if !SWATTN_PW_QGLOBAL
   uint8_t q[kQBytes];
+#endif
 };
 struct __align__(1024) PwSmem {
   WarpSmem w[kWarps];
@@ -196,14 +205,18 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     ++issued;
     prod.advance(p, lane);
   };
+#if !SWATTN_PW_QGLOBAL
   if (lane == 0) {
     tc::mbar_arrive_expect_tx(qfull, kQBytes);
     tc::tma_load_4d(&p.q_map, qfull, ws.q, 0, prod.g * kG, 0, (int)prod.t);
   }
+#endif
   for (int i = 0; i < kStages && prod.valid(p); ++i) issue();
 
   const uint32_t kbase = tc::smem_u32(ws.k[0]), vbase = tc::smem_u32(ws.v[0]);
+#if !SWATTN_PW_QGLOBAL
   const uint32_t qaddr = tc::smem_u32(ws.q);
+#endif
   const int h0 = lane >> 2;  // rows (heads) h0 and h0 + 8 of every fragment
   // ldmatrix lane roles: matrix m = lane / 8, row-in-matrix = lane % 8
   const int lm = lane >> 3, lr = lane & 7;
@@ -216,9 +229,23 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     const int64_t row = (int64_t)cons.g * p.n + cons.t;
     const int64_t ridx = cons.t * p.h_q + cons.g * kG;  // [n][h_q] row of head 0
     // ---- Q fragments (A operand, 16 heads x 128 d) for the whole token
+    uint32_t qa[8][4];
+#if SWATTN_PW_QGLOBAL
+    {
+      // a0 = (head h0, d 16 ks + 2 (lane & 3)), a1 = head h0 + 8, a2/a3 = d + 8
+      const uint32_t *qg = reinterpret_cast<const uint32_t *>(p.Q + ridx * kD);
+      const int dw = lane & 3;  // 32-bit word within the 8-column group
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        qa[ks][0] = __ldg(qg + h0 * (kD / 2) + ks * 8 + dw);
+        qa[ks][1] = __ldg(qg + (h0 + 8) * (kD / 2) + ks * 8 + dw);
+        qa[ks][2] = __ldg(qg + h0 * (kD / 2) + ks * 8 + 4 + dw);
+        qa[ks][3] = __ldg(qg + (h0 + 8) * (kD / 2) + ks * 8 + 4 + dw);
+      }
+    }
+#else
     tc::mbar_wait(qfull, (uint32_t)(qphase & 1));
     ++qphase;
-    uint32_t qa[8][4];
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       // matrices: (heads 0-7, d lo), (heads 8-15, d lo), (heads 0-7, d hi), (heads 8-15, d hi)
@@ -237,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
         tc::tma_load_4d(&p.q_map, qfull, ws.q, 0, nx.g * kG, 0, (int)nx.t);
       }
     }
+#endif
     const float mA0 = p.m_a[ridx + h0], mA1 = p.m_a[ridx + h0 + 8];
     float lp0 = 0.f, lp1 = 0.f, excess = -INFINITY;
     float o[16][4];
@@ -373,6 +401,7 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
   p.topk_cnt = topk_cnt;
   p.m_a = m_a;
   p.l_a = l_a;
+  p.Q = static_cast<const __nv_bfloat16 *>(Q);
   p.O = static_cast<__nv_bfloat16 *>(O);
   p.lse = lse;
   p.scale_log2 = (1.f / sqrtf((float)cfg->d_h)) * 1.4426950408889634f;
