@@ -298,14 +298,15 @@ def run_ours(args):
             "stages_ms": stages,
             "k4_gather": {"bytes": _gather_bytes(cfg, n),
                           "achieved_TBs_over_K4": _gather_bytes(cfg, n) / (stages["K4_sparse_attention"] / 1e3) / 1e12,
-                          "l2_gather_peak_TBs": 19.6,
-                          "peak_source": "tools/gather_bench.cu, 4 TMA issuer warps x 2 CTAs/SM (measured)"},
+                          "l2_gather_peak_TBs": 19.7,
+                          "peak_source": "tools/gather_bench.cu SM sweep: 133 GB/s per SM x 148 SMs, "
+                                         "bound per SM (profiles/r01c_gather_sm_sweep.txt)"},
             "e2e": {"value": ws * n / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            # per attend: compress, scores_tc, topk, rerank, fa_tile (part A),
-            # sparse_pw (part B), attention_list (overflow rows) -- see the
-            # committed ncu launch list under profiles/
-            "gpu_launches": args.steps * 7,
+            # per attend: compress, scores_tc, topk, rerank_p1, rerank,
+            # fa_tile (part A), sparse_pw (part B), attention_list (overflow
+            # rows) -- see the committed ncu launch list under profiles/
+            "gpu_launches": args.steps * 8,
             "dense_comparator": dense,
             "clocks": clk.summary(),
         }

@@ -47,6 +47,15 @@ constexpr uint32_t kQBytes = kRows * kD * 2;      // 32 KB
 constexpr uint32_t kKBytes = kCols * kD * 2;      // 32 KB
 constexpr uint32_t kTmemCols = 256;
 
+// heads 0, 4, .. 4 (SWATTN_K2_POLY_GROUPS - 1) of every 16 take their pass-2
+// exp on the FMA pipe (0 = all on MUFU)
+#ifndef SWATTN_K2_POLY_GROUPS
+#define SWATTN_K2_POLY_GROUPS 2  // measured best: 8.09 -> 7.39 ms at 128K (tools/probe_partb.sh pf1-3)
+#endif
+// pass 1: every 8th column's exp on the FMA pipe as well
+#ifndef SWATTN_K2_POLY_P1
+#define SWATTN_K2_POLY_P1 0
+#endif
 // timing-decomposition switches for variant builds (tools/build_variants.sh)
 #ifdef SWATTN_K2_NO_EXP
 #define K2_EXP(x) (x)
@@ -229,7 +238,8 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
       for (int e = 0; e < 64; e += 4) {
-        a0 += fast_exp2(fmaf(x[e], p.scale_log2, -m));
+        const float y0 = fmaf(x[e], p.scale_log2, -m);
+        a0 += (SWATTN_K2_POLY_P1 && e % 8 == 0) ? poly_exp2(y0) : fast_exp2(y0);
         a1 += fast_exp2(fmaf(x[e + 1], p.scale_log2, -m));
         a2 += fast_exp2(fmaf(x[e + 2], p.scale_log2, -m));
         a3 += fast_exp2(fmaf(x[e + 3], p.scale_log2, -m));
@@ -277,7 +287,10 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
             const uint32_t u1 = cidx + 1 < 32 ? va[cidx + 1] : vb[cidx + 1 - 32];
             const uint32_t u2 = cidx + 2 < 32 ? va[cidx + 2] : vb[cidx + 2 - 32];
             const uint32_t u3 = cidx + 3 < 32 ? va[cidx + 3] : vb[cidx + 3 - 32];
-            a0 = fmaf(K2_EXP(fmaf(__uint_as_float(u0), p.scale_log2, -st01.x)), st01.y, a0);
+            // heads offloaded to the FMA pipe (poly_exp2) relieve MUFU, the
+            // bound of this epilogue
+            const float x0 = fmaf(__uint_as_float(u0), p.scale_log2, -st01.x);
+            a0 = fmaf(((h / 4) < SWATTN_K2_POLY_GROUPS) ? poly_exp2(x0) : K2_EXP(x0), st01.y, a0);
             a1 = fmaf(K2_EXP(fmaf(__uint_as_float(u1), p.scale_log2, -st01.z)), st01.w, a1);
             a2 = fmaf(K2_EXP(fmaf(__uint_as_float(u2), p.scale_log2, -st23.x)), st23.y, a2);
             a3 = fmaf(K2_EXP(fmaf(__uint_as_float(u3), p.scale_log2, -st23.z)), st23.w, a3);

@@ -124,6 +124,30 @@ def chunk_rows_for(n: int, B: int) -> int:
     return -(-rows // B) * B
 
 
+def chunk_bounds(n: int, B: int, rows: int | None = None) -> list[tuple[int, int]]:
+    """Row chunks of the host pipeline.  With the default size the first and
+    last chunks are short (2048 rows): the first one's Q arrives quickly
+    (compute starts after K, V and 16 MB of Q instead of 67 MB), and the
+    last one's O / lse leave quickly (the copy tail after the final kernel)."""
+    if rows is not None:
+        return [(r, min(n, r + rows)) for r in range(0, n, rows)]
+    rows = chunk_rows_for(n, B)
+    edge = -(-2048 // B) * B
+    if n < 4 * rows:
+        return [(r, min(n, r + rows)) for r in range(0, n, rows)]
+    last0 = (n - edge) // B * B               # start of the short last chunk
+    bounds = [(0, edge)]
+    mid = last0 - edge
+    k = max(1, round(mid / rows))
+    step = -(-(-(-mid // k)) // B) * B
+    r = edge
+    while r < last0:
+        bounds.append((r, min(last0, r + step)))
+        r += step
+    bounds.append((last0, n))
+    return bounds
+
+
 def attend_host_chunked(Q, K, V, cfg: AttentionConfig, selection_mode: str = "approx",
                         out=None, chunk_rows: int | None = None, device=None):
     """Sparse branch of attend for HOST inputs with the host<->device copies
@@ -151,8 +175,7 @@ def attend_host_chunked(Q, K, V, cfg: AttentionConfig, selection_mode: str = "ap
     ws = Workspace.get(L.swattn_workspace_bytes(c, n), device)
     comp = torch.cuda.current_stream(device)
     s_in, s_out = st["in"], st["out"]
-    rows = chunk_rows or chunk_rows_for(n, cfg.B)
-    bounds = [(r, min(n, r + rows)) for r in range(0, n, rows)]
+    bounds = chunk_bounds(n, cfg.B, chunk_rows)
     s_in.wait_stream(comp)   # device buffers may still be read by the previous call
     s_out.wait_stream(comp)
     with torch.cuda.stream(s_in):
