@@ -147,6 +147,19 @@ int32_t swattn_attend(const swattn_config *cfg, const void *Q, const void *K, co
                       void *O, float *lse, int32_t *mode_taken, void *workspace,
                       size_t workspace_bytes, void *stream);
 
+/* sparse_backward (sparse.py:130-185): dQ [n,h_q,d_h], dK / dV [n,h_kv,d_h]
+ * bf16 of sum(O * dO) through the masked softmax over each row's init U local
+ * U top-k blocks, given the forward's O (bf16) and lse (fp32, natural log) --
+ * e.g. from swattn_sparse_fwd -- and dO (bf16).  Deterministic: every
+ * reduction has a fixed order.  One host synchronisation (the data-dependent
+ * pair count).  Paper profile only (SWATTN_EUNSUPPORTED otherwise). */
+int32_t swattn_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K,
+                          const void *V, int64_t n, const int32_t *topk,
+                          const int32_t *topk_cnt, const void *O, const float *lse,
+                          const void *dO, void *dQ, void *dK, void *dV, void *workspace,
+                          size_t workspace_bytes, void *stream);
+size_t swattn_sparse_bwd_workspace_bytes(const swattn_config *cfg, int64_t n);
+
 /* ---- row ranges (copy-overlapped chunked prefill) ----
  * The same computations restricted to query rows [r0, r1) of an n-token
  * sequence: r0 and r1 are multiples of B (r1 may equal n).  Rows only read

@@ -65,7 +65,7 @@ def main():
     paper = AttentionConfig()
 
     def case(name, cfg, n, seed, *, scores=False, exact=False, sparse_rows=None,
-             dense_rows=None, forced=None):
+             dense_rows=None, forced=None, backward_rows=None):
         if args.only and args.only not in name:
             return
         t0 = time.time()
@@ -109,6 +109,20 @@ def main():
             rec["dense_rows"] = rows
             rec["dense_out_bits"] = _bits(res.output[rows])
             rec["dense_lse"] = res.lse[rows]
+        if backward_rows is not None:
+            # sparse_backward (sparse.py:130-185) with dO = the Q of seed + 1000
+            from swattn.sparse import sparse_backward
+            dO, _, _ = make_qkv(n, cfg.h_q, cfg.h_kv, cfg.d_h, seed=seed + 1000, dtype=bf)
+            dQ, dK, dV = sparse_backward(Q, K, V, sel, dO, cfg)
+            rows = np.asarray(backward_rows)
+            rec["bwd_rows"] = rows
+            rec["bwd_dQ_bits"] = _bits(dQ[rows])
+            krows = rows if n <= 512 else np.unique(np.concatenate([
+                rows, np.arange(0, 64), np.arange(n - 64, n)]))   # block 0 gets every query
+            rec["bwd_key_rows"] = krows
+            rec["bwd_dK_bits"] = _bits(dK[krows])
+            rec["bwd_dV_bits"] = _bits(dV[krows])
+            rec["bwd_digest"] = digest(dQ, dK, dV)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **rec)
         print(f"{name}: {time.time() - t0:.1f}s -> {os.path.getsize(path) / 1e6:.2f} MB",
@@ -129,6 +143,10 @@ def main():
     # paper profile (core.py:78-91)
     case("paper_n300_s5", paper, 300, 5, scores=True, sparse_rows=sample(300, 40, 6),
          dense_rows=sample(300, 40, 7))
+    # backward (sparse.py:130-185): small profile, and the paper profile at
+    # a length where top-k is competitive (n > 96 blocks * 64)
+    case("bwd_small_n257_s0", small, 257, 0, backward_rows=np.arange(257))
+    case("bwd_paper_n7000_s8", paper, 7000, 8, backward_rows=sample(7000, 24, 9))
     case("paper_n4096_s0", paper, 4096, 0, sparse_rows=sample(4096, 96, 0),
          dense_rows=sample(4096, 96, 1))
     case("paper_n8192_s0", paper, 8192, 0, scores=True, exact=True,

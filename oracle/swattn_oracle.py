@@ -313,6 +313,49 @@ def sparse_attention(Q, K, V, topk: np.ndarray, cfg: Profile, rows=None, out_dty
     return O, L
 
 
+def sparse_backward(Q, K, V, topk: np.ndarray, dO, cfg: Profile, rows=None):
+    """Gradients of sum(O * dO) through the masked softmax (sparse.py:130-185).
+
+    The forward is recomputed in float64 (sparse.py:157-158), delta = rowsum
+    dO * O (:169), and per row the visible keys give P = exp(S - lse),
+    dP = dO V^T, dS = P (dP - delta), dQ = dS K scale, dK += dS^T Q scale,
+    dV += P^T dO (:171-180).  The reference walks spans in ascending order;
+    here all visible keys of a row are one matrix product (same sums in
+    float64, different association).  dQ is returned for `rows` (all rows by
+    default); dK / dV accumulate the contributions of `rows` only (complete
+    for rows=None).  Returns float64 (dQ [R, h_q, d], dK [n, h_kv, d],
+    dV [n, h_kv, d]); the reference casts to the storage dtype (:185)."""
+    n = Q.shape[0]
+    rows = np.arange(n) if rows is None else np.asarray(rows, dtype=np.int64)
+    G = cfg.G
+    scale = 1.0 / np.sqrt(cfg.d_h)
+    K64 = K.astype(np.float64)
+    V64 = V.astype(np.float64)
+    dQ = np.zeros((rows.size, cfg.h_q, cfg.d_h))
+    dK = np.zeros((n, cfg.h_kv, cfg.d_h))
+    dV = np.zeros((n, cfg.h_kv, cfg.d_h))
+    for ri, i in enumerate(rows):
+        for g in range(cfg.h_kv):
+            blocks = full_block_set(topk[g, i], int(i), cfg)
+            keys = np.flatnonzero(token_mask_row(int(i), blocks, n, cfg.B))
+            q = Q[i, g * G:(g + 1) * G].astype(np.float64)
+            do = dO[i, g * G:(g + 1) * G].astype(np.float64)
+            S = (q @ K64[keys, g].T) * scale
+            mx = S.max(axis=1)
+            z = np.exp(S - mx[:, None])
+            ell = z.sum(axis=1)
+            lse = mx + np.log(ell)
+            P = np.exp(S - lse[:, None])
+            O = P @ V64[keys, g]
+            delta = (do * O).sum(axis=1)
+            dP = do @ V64[keys, g].T
+            dS = P * (dP - delta[:, None])
+            dQ[ri, g * G:(g + 1) * G] = (dS @ K64[keys, g]) * scale
+            dK[keys, g] += (dS.T @ q) * scale
+            dV[keys, g] += P.T @ do
+    return dQ, dK, dV
+
+
 def dense_attention(Q, K, V, cfg: Profile, rows=None, causal: bool = True, out_dtype=None):
     """Causal GQA softmax attention, float64 (dense.py:64-109; the tiled
     form dense.py:112-170 computes the same values)."""

@@ -63,3 +63,48 @@ def token_visibility_mask(sel: BlockSelection, g: int):
         for start, end in sel.visible_spans(g, i):
             mask[i, start:end] = True
     return mask
+
+
+def sparse_backward(Q, K, V, sel: BlockSelection, dO, cfg: AttentionConfig,
+                    counter: OpCounter | None = None):
+    """sparse.py:130-185 on the GPU: gradients of sum(O * dO) through the
+    masked softmax, recomputing P from the forward's lse (the forward runs
+    first, as in the reference, :157-158).  dK / dV reduce in a fixed order
+    (bitwise reproducible, :139-143).  Returns (dQ, dK, dV) in Q's storage
+    dtype (bf16 tensors on the device for device inputs, numpy bf16 for host
+    inputs)."""
+    n, h_q, h_kv, d_h = check_gqa_shapes(Q, K, V, cfg)
+    _check_selection(sel, n, h_kv)
+    if tuple(dO.shape) != tuple(Q.shape):
+        raise ValueError(f"dO shape {tuple(dO.shape)} != Q shape {tuple(Q.shape)}")
+    host = is_host(Q)
+    Qd, Kd, Vd, dOd = (to_device_bf16(x, nm) for x, nm in ((Q, "Q"), (K, "K"), (V, "V"),
+                                                          (dO, "dO")))
+    fwd = sparse_forward(Qd, Kd, Vd, sel, cfg)
+    dQ = torch.empty_like(Qd)
+    dK = torch.empty_like(Kd)
+    dV = torch.empty_like(Vd)
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    nbytes = L.swattn_sparse_bwd_workspace_bytes(c, n)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=Qd.device)
+    topk = sel.topk.contiguous()
+    _lib.check(L.swattn_sparse_bwd(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), n,
+                                   topk.data_ptr(), sel.topk_cnt.data_ptr(),
+                                   fwd.output.data_ptr(), fwd.lse.data_ptr(), dOd.data_ptr(),
+                                   dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), _lib.stream_handle(Qd.device)),
+               "swattn_sparse_bwd")
+    if counter is not None:
+        cnt = sel.topk_cnt.to(torch.int64)
+        i = torch.arange(n, device=cnt.device)
+        b = i // cfg.B
+        picked = torch.clamp(b + 1, max=cfg.N_init + cfg.N_local) + cnt
+        visits = int(((picked - 1) * cfg.B + (i - b * cfg.B) + 1).sum())
+        counter.add(mac=4 * visits * (h_q // h_kv) * d_h, exp=visits * (h_q // h_kv))
+    if host:
+        import ml_dtypes
+        import numpy as np
+        return tuple(t.cpu().view(torch.int16).numpy().view(ml_dtypes.bfloat16)
+                     for t in (dQ, dK, dV))
+    return dQ, dK, dV

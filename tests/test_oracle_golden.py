@@ -108,3 +108,25 @@ def test_spec_known_answers():
     cfg = O.PAPER
     assert (cfg.N_init + cfg.N_local + cfg.k_top) * cfg.B == 6144
     assert O.sparse_visible_tokens(32767, cfg) == 6144
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith("bwd_")])
+def test_backward_matches_reference(name):
+    """sparse_backward (sparse.py:130-185) with dO = make_qkv(seed + 1000).Q:
+    dQ on the stored rows; dK / dV on the stored key rows when the oracle can
+    afford every query row (small n)."""
+    rec = load_golden(name)
+    cfg, Q, K, V = _inputs(rec)
+    n = int(rec["n"])
+    dO, _, _ = O.draw_qkv(n, cfg.h_q, cfg.h_kv, cfg.d_h, int(rec["seed"]) + 1000)
+    top = rec["topk"].astype(np.int64)
+    top = np.concatenate([top, np.full(top.shape[:2] + (cfg.k_top - top.shape[2],), -1)], 2) \
+        if top.shape[2] < cfg.k_top else top
+    rows = rec["bwd_rows"]
+    full = n <= 512
+    dQ, dK, dV = O.sparse_backward(Q, K, V, top, dO, cfg, rows=None if full else rows)
+    _bf16_close(dQ[rows] if full else dQ, rec["bwd_dQ_bits"])
+    if full:
+        kr = rec["bwd_key_rows"]
+        _bf16_close(dK[kr], rec["bwd_dK_bits"])
+        _bf16_close(dV[kr], rec["bwd_dV_bits"])
