@@ -159,6 +159,14 @@ int32_t swattn_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
                           const void *dO, void *dQ, void *dK, void *dV, void *workspace,
                           size_t workspace_bytes, void *stream);
 size_t swattn_sparse_bwd_workspace_bytes(const swattn_config *cfg, int64_t n);
+/* naive_gqa_backward (dense.py:173-221): the same kernels with every causal
+ * block (causal = 1) or every block (causal = 0) visible; O / lse from
+ * swattn_dense_fwd with the same causal flag. */
+int32_t swattn_dense_bwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                         int64_t n, int32_t causal, const void *O, const float *lse,
+                         const void *dO, void *dQ, void *dK, void *dV, void *workspace,
+                         size_t workspace_bytes, void *stream);
+size_t swattn_dense_bwd_workspace_bytes(const swattn_config *cfg, int64_t n, int32_t causal);
 
 /* ---- row ranges (copy-overlapped chunked prefill) ----
  * The same computations restricted to query rows [r0, r1) of an n-token

@@ -65,7 +65,7 @@ def main():
     paper = AttentionConfig()
 
     def case(name, cfg, n, seed, *, scores=False, exact=False, sparse_rows=None,
-             dense_rows=None, forced=None, backward_rows=None):
+             dense_rows=None, forced=None, backward_rows=None, dense_backward=False):
         if args.only and args.only not in name:
             return
         t0 = time.time()
@@ -123,6 +123,14 @@ def main():
             rec["bwd_dK_bits"] = _bits(dK[krows])
             rec["bwd_dV_bits"] = _bits(dV[krows])
             rec["bwd_digest"] = digest(dQ, dK, dV)
+        if dense_backward:
+            # naive_gqa_backward (dense.py:173-221), dO = the Q of seed + 1000
+            from swattn.dense import naive_gqa_backward
+            dO, _, _ = make_qkv(n, cfg.h_q, cfg.h_kv, cfg.d_h, seed=seed + 1000, dtype=bf)
+            dQ, dK, dV = naive_gqa_backward(Q, K, V, dO, cfg)
+            rec["dbwd_dQ_bits"] = _bits(dQ)
+            rec["dbwd_dK_bits"] = _bits(dK)
+            rec["dbwd_dV_bits"] = _bits(dV)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **rec)
         print(f"{name}: {time.time() - t0:.1f}s -> {os.path.getsize(path) / 1e6:.2f} MB",
@@ -146,6 +154,7 @@ def main():
     # backward (sparse.py:130-185): small profile, and the paper profile at
     # a length where top-k is competitive (n > 96 blocks * 64)
     case("bwd_small_n257_s0", small, 257, 0, backward_rows=np.arange(257))
+    case("bwd_dense_paper_n200_s4", paper, 200, 4, dense_backward=True)
     case("bwd_paper_n7000_s8", paper, 7000, 8, backward_rows=sample(7000, 24, 9))
     case("paper_n4096_s0", paper, 4096, 0, sparse_rows=sample(4096, 96, 0),
          dense_rows=sample(4096, 96, 1))

@@ -356,6 +356,35 @@ def sparse_backward(Q, K, V, topk: np.ndarray, dO, cfg: Profile, rows=None):
     return dQ, dK, dV
 
 
+def dense_backward(Q, K, V, dO, cfg: Profile, causal: bool = True):
+    """naive_gqa_backward (dense.py:173-221): per head h (KV head h // G),
+    P = softmax(QK^T scale, causal), dV += P^T dO, dP = dO V^T,
+    delta = rowsum(dP * P), dS = P (dP - delta), dQ = dS K scale,
+    dK += dS^T Q scale; float64.  Returns (dQ, dK, dV)."""
+    n = Q.shape[0]
+    G = cfg.G
+    scale = 1.0 / np.sqrt(cfg.d_h)
+    Q64, K64, V64, dO64 = (x.astype(np.float64) for x in (Q, K, V, dO))
+    fut = np.triu(np.ones((n, n), dtype=bool), k=1) if causal else None
+    dQ = np.zeros((n, cfg.h_q, cfg.d_h))
+    dK = np.zeros((n, cfg.h_kv, cfg.d_h))
+    dV = np.zeros((n, cfg.h_kv, cfg.d_h))
+    for h in range(cfg.h_q):
+        kv = h // G
+        S = (Q64[:, h] @ K64[:, kv].T) * scale
+        if causal:
+            S[fut] = -np.inf
+        P = np.exp(S - S.max(axis=1)[:, None])
+        P /= P.sum(axis=1)[:, None]
+        dV[:, kv] += P.T @ dO64[:, h]
+        dP = dO64[:, h] @ V64[:, kv].T
+        delta = (dP * P).sum(axis=1)
+        dS = P * (dP - delta[:, None])
+        dQ[:, h] = (dS @ K64[:, kv]) * scale
+        dK[:, kv] += (dS.T @ Q64[:, h]) * scale
+    return dQ, dK, dV
+
+
 def dense_attention(Q, K, V, cfg: Profile, rows=None, causal: bool = True, out_dtype=None):
     """Causal GQA softmax attention, float64 (dense.py:64-109; the tiled
     form dense.py:112-170 computes the same values)."""

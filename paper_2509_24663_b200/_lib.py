@@ -82,6 +82,8 @@ def lib():
         "swattn_sparse_workspace_bytes": (SZ, [cfgp, I64]),
         "swattn_sparse_bwd": (I32, [cfgp, P, P, P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
         "swattn_sparse_bwd_workspace_bytes": (SZ, [cfgp, I64]),
+        "swattn_dense_bwd": (I32, [cfgp, P, P, P, I64, I32, P, P, P, P, P, P, P, SZ, P]),
+        "swattn_dense_bwd_workspace_bytes": (SZ, [cfgp, I64, I32]),
         "swattn_dense_fwd": (I32, [cfgp, P, P, P, I64, I32, P, P, P]),
         "swattn_attend": (I32, [cfgp, P, P, P, I64, I64, I32, I32, P, P,
                                 ctypes.POINTER(I32), P, SZ, P]),
@@ -107,6 +109,7 @@ EXPORTED = (
     "swattn_num_pooled", "swattn_workspace_bytes", "swattn_compress_keys", "swattn_block_scores",
     "swattn_shared_scores", "swattn_topk_blocks", "swattn_select_blocks", "swattn_sparse_fwd",
     "swattn_sparse_workspace_bytes", "swattn_sparse_bwd", "swattn_sparse_bwd_workspace_bytes",
+    "swattn_dense_bwd", "swattn_dense_bwd_workspace_bytes",
     "swattn_dense_fwd", "swattn_attend", "swattn_select_blocks_rows", "swattn_sparse_fwd_rows",
     "swattn_attend_rows", "swattn_attend_prepare", "swattn_workspace_ckeys", "swattn_kcache_append", "swattn_decode_step",
     "swattn_decode_workspace_bytes",

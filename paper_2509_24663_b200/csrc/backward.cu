@@ -100,9 +100,19 @@ struct RowBlocks {
   int lo, nl, ni, nt;
   __device__ int count() const { return nl + ni + nt; }
 };
-__device__ __forceinline__ RowBlocks row_blocks(int64_t i, int B, int N_init, int N_local, int cnt) {
+// mode: 0 sparse (init U local U top-k), 1 dense causal ([0, b]), 2 dense
+// non-causal (every block of the nb) -- dense.py:173-221
+__device__ __forceinline__ RowBlocks row_blocks(int64_t i, int B, int N_init, int N_local, int cnt,
+                                                int mode = 0, int nb = 0) {
   RowBlocks r;
   const int b = (int)(i / B);
+  if (mode != 0) {
+    r.lo = 0;
+    r.nl = mode == 1 ? b + 1 : nb;
+    r.ni = 0;
+    r.nt = 0;
+    return r;
+  }
   r.lo = max(0, b - N_local + 1);
   r.nl = b - r.lo + 1;
   r.ni = min(N_init, r.lo);
@@ -139,7 +149,7 @@ struct DqParams {
   const int32_t *topk, *topk_cnt;
   __nv_bfloat16 *dQ;
   int64_t n;
-  int h_q, h_kv, k_top, B, N_init, N_local;
+  int h_q, h_kv, k_top, B, N_init, N_local, mode, nb;
   float scale, scale_log2;
 };
 
@@ -164,8 +174,8 @@ struct DqStream {
       g = (int)(it / p.n);
       t = it % p.n;
       const int64_t row = (int64_t)g * p.n + t;
-      rb = row_blocks(t, p.B, p.N_init, p.N_local, p.topk_cnt[row]);
-      const int32_t *tk = p.topk + row * p.k_top;
+      rb = row_blocks(t, p.B, p.N_init, p.N_local, p.mode == 0 ? p.topk_cnt[row] : 0, p.mode, p.nb);
+      const int32_t *tk = p.topk + (p.mode == 0 ? row * p.k_top : 0);
       id0 = lane < rb.nt ? tk[lane] : 0;
       id1 = lane + 32 < rb.nt ? tk[lane + 32] : 0;
       s = 0;
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) bwd_dq_kernel(const __grid_co
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int64_t key = key0 + j * 8 + 2 * (lane & 3) + (e & 1);
-          const bool vis = key <= t && key < p.n;
+          const bool vis = (p.mode == 2 || key <= t) && key < p.n;
           const float lse2 = e < 2 ? l0 : l1, dl = e < 2 ? d0 : d1;
           const float pr = vis ? fast_exp2(fmaf(sc[j][e], p.scale_log2, -lse2)) : 0.f;
           ds[j][e] = pr * (dp[j][e] - dl);
@@ -313,16 +323,17 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) bwd_dq_kernel(const __grid_co
 
 // ------------------------------------------------------------------ B2
 // key = (g * nb + block) << 32 | query
-__global__ void bwd_pair_count_kernel(int64_t n, int h_kv, int B, int N_init, int N_local,
-                                      const int32_t *__restrict__ topk_cnt, int64_t *__restrict__ cnt) {
+__global__ void bwd_pair_count_kernel(int64_t n, int h_kv, int B, int N_init, int N_local, int mode,
+                                      int nb, const int32_t *__restrict__ topk_cnt,
+                                      int64_t *__restrict__ cnt) {
   const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (it >= (int64_t)h_kv * n) return;
   const int64_t i = it % n;
-  cnt[it] = row_blocks(i, B, N_init, N_local, topk_cnt[it]).count();
+  cnt[it] = row_blocks(i, B, N_init, N_local, mode == 0 ? topk_cnt[it] : 0, mode, nb).count();
 }
 
 __global__ void bwd_pair_fill_kernel(int64_t n, int h_kv, int B, int N_init, int N_local, int k_top,
-                                     int64_t nb, const int32_t *__restrict__ topk,
+                                     int mode, int64_t nb, const int32_t *__restrict__ topk,
                                      const int32_t *__restrict__ topk_cnt,
                                      const int64_t *__restrict__ off, uint64_t *__restrict__ keys,
                                      int32_t *__restrict__ blk_count) {
@@ -330,9 +341,9 @@ __global__ void bwd_pair_fill_kernel(int64_t n, int h_kv, int B, int N_init, int
   if (it >= (int64_t)h_kv * n) return;
   const int g = (int)(it / n);
   const int64_t i = it % n;
-  const RowBlocks rb = row_blocks(i, B, N_init, N_local, topk_cnt[it]);
+  const RowBlocks rb = row_blocks(i, B, N_init, N_local, mode == 0 ? topk_cnt[it] : 0, mode, (int)nb);
   uint64_t *out = keys + off[it];
-  const int32_t *tk = topk + it * k_top;
+  const int32_t *tk = topk + (mode == 0 ? it * k_top : 0);
   const int c = rb.count();
   for (int j = 0; j < c; ++j) {
     int blk;
@@ -385,7 +396,7 @@ struct DkvParams {
   const int32_t *n_segs;  // device total
   float *part;            // [segment][2][64][128] fp32 (dK, dV partials)
   int64_t n, nb;
-  int h_q, h_kv;
+  int h_q, h_kv, mode;
   float scale_log2;
 };
 
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
       for (int e = 0; e < 4; ++e) {
         const int h = j * 8 + 2 * (lane & 3) + (e & 1);
         const int64_t key = key_w + (lane >> 2) + (e >= 2 ? 8 : 0);
-        const bool vis = key <= i && key < p.n;
+        const bool vis = (p.mode == 2 || key <= i) && key < p.n;
         const float pr = vis ? fast_exp2(fmaf(st[j][e], p.scale_log2, -sm.lse[buf][h])) : 0.f;
         pt[j][e] = pr;
         dst[j][e] = pr * (dpt[j][e] - sm.delta[buf][h]);
@@ -548,12 +559,13 @@ struct BwdLayout {
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-BwdLayout bwd_layout(const swattn_config *cfg, int64_t n) {
+BwdLayout bwd_layout(const swattn_config *cfg, int64_t n, int mode) {
   BwdLayout L{};
   L.items = (int64_t)cfg->h_kv * n;
   L.nb = cdiv(n, cfg->B);
   L.n_gb = (int64_t)cfg->h_kv * L.nb;
-  const int64_t per_row = cfg->N_init + cfg->N_local + cfg->k_top;
+  const int64_t per_row = mode == 0 ? std::min<int64_t>(cfg->N_init + cfg->N_local + cfg->k_top, L.nb)
+                                    : L.nb;
   L.max_pairs = L.items * per_row;
   L.max_segs = L.max_pairs / kSeg + L.n_gb + 1;
   // CUB temp storage (queried with null buffers; no device work)
@@ -589,15 +601,17 @@ __global__ void bwd_total_segs_kernel(const int32_t *seg_off, const int32_t *nse
 
 }  // namespace
 
-size_t sparse_bwd_workspace_bytes(const swattn_config *cfg, int64_t n) {
-  return bwd_layout(cfg, n).total;
+size_t sparse_bwd_workspace_bytes(const swattn_config *cfg, int64_t n, int mode) {
+  return bwd_layout(cfg, n, mode).total;
 }
 
+// mode 0: sparse (topk / topk_cnt), 1: dense causal, 2: dense non-causal
 int32_t launch_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                           int64_t n, const int32_t *topk, const int32_t *topk_cnt, const void *O,
                           const float *lse, const void *dO, void *dQ, void *dK, void *dV,
-                          void *workspace, size_t workspace_bytes, int num_sms, cudaStream_t st) {
-  const BwdLayout L = bwd_layout(cfg, n);
+                          void *workspace, size_t workspace_bytes, int num_sms, int mode,
+                          cudaStream_t st) {
+  const BwdLayout L = bwd_layout(cfg, n, mode);
   if (workspace == nullptr || workspace_bytes < L.total) {
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, L.total);
     return SWATTN_EINVAL;
@@ -651,6 +665,8 @@ int32_t launch_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
     p.B = cfg->B;
     p.N_init = cfg->N_init;
     p.N_local = cfg->N_local;
+    p.mode = mode;
+    p.nb = (int)L.nb;
     p.scale = scale;
     p.scale_log2 = scale * kLog2e;
     const size_t smem = sizeof(DqSmem) + 1024;
@@ -668,7 +684,7 @@ int32_t launch_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
   {
     const unsigned g1 = (unsigned)cdiv(L.items, 256);
     bwd_pair_count_kernel<<<g1, 256, 0, st>>>(n, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local,
-                                              topk_cnt, cnt);
+                                              mode, (int)L.nb, topk_cnt, cnt);
     SWATTN_LAUNCH_CHECK("bwd_pair_count_kernel");
     size_t tb = L.temp_bytes;
     if ((rc = cuda_check(cub::DeviceScan::ExclusiveSum(temp, tb, cnt, off, (int)L.items, st), "scan(pairs)")))
@@ -676,7 +692,8 @@ int32_t launch_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
     if ((rc = cuda_check(cudaMemsetAsync(blk_count, 0, (size_t)(L.n_gb + 1) * 4, st), "memset")))
       return rc;
     bwd_pair_fill_kernel<<<g1, 256, 0, st>>>(n, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local,
-                                             cfg->k_top, L.nb, topk, topk_cnt, off, keys, blk_count);
+                                             cfg->k_top, mode, L.nb, topk, topk_cnt, off, keys,
+                                             blk_count);
     SWATTN_LAUNCH_CHECK("bwd_pair_fill_kernel");
     // the pair count is data-dependent (top-k counts): sort the max_pairs
     // buffer? no -- sort exactly the filled prefix, whose length is off[items-1]
@@ -723,6 +740,7 @@ int32_t launch_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
     q.nb = L.nb;
     q.h_q = cfg->h_q;
     q.h_kv = cfg->h_kv;
+    q.mode = mode;
     q.scale_log2 = scale * kLog2e;
     const int64_t max_segs = npairs / kSeg + L.n_gb + 1;
     bwd_dkdv_kernel<<<(unsigned)max_segs, kKvWarps * 32, 0, st>>>(q);

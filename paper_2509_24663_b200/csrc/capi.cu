@@ -60,8 +60,8 @@ int32_t launch_attention_list(const swattn_config *, const void *, const void *,
                               const int32_t *, void *, float *, int, cudaStream_t);
 int32_t launch_sparse_bwd(const swattn_config *, const void *, const void *, const void *, int64_t,
                           const int32_t *, const int32_t *, const void *, const float *, const void *,
-                          void *, void *, void *, void *, size_t, int, cudaStream_t);
-size_t sparse_bwd_workspace_bytes(const swattn_config *, int64_t);
+                          void *, void *, void *, void *, size_t, int, int, cudaStream_t);
+size_t sparse_bwd_workspace_bytes(const swattn_config *, int64_t, int);
 int32_t launch_dense_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
                         int, void *, float *, cudaStream_t);
 bool scores_tc_available();
@@ -584,7 +584,31 @@ int32_t swattn_sparse_fwd_rows(const swattn_config *cfg, const void *Q, const vo
 
 size_t swattn_sparse_bwd_workspace_bytes(const swattn_config *cfg, int64_t n) {
   if (cfg == nullptr || n < 1 || !swattn_profile_supported(cfg)) return 0;
-  return sparse_bwd_workspace_bytes(cfg, n);
+  return sparse_bwd_workspace_bytes(cfg, n, 0);
+}
+
+size_t swattn_dense_bwd_workspace_bytes(const swattn_config *cfg, int64_t n, int32_t causal) {
+  if (cfg == nullptr || n < 1 || !swattn_profile_supported(cfg)) return 0;
+  return sparse_bwd_workspace_bytes(cfg, n, causal ? 1 : 2);
+}
+
+int32_t swattn_dense_bwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                         int64_t n, int32_t causal, const void *O, const float *lse, const void *dO,
+                         void *dQ, void *dK, void *dV, void *workspace, size_t workspace_bytes,
+                         void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  if (!swattn_profile_supported(cfg) || !use_tc_attention()) {
+    set_error("unsupported profile for the backward kernels (need the paper profile)");
+    return SWATTN_EUNSUPPORTED;
+  }
+  return launch_sparse_bwd(cfg, Q, K, V, n, nullptr, nullptr, O, lse, dO, dQ, dK, dV, workspace,
+                           workspace_bytes, num_sms(), causal ? 1 : 2,
+                           static_cast<cudaStream_t>(stream));
 }
 
 int32_t swattn_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,
@@ -606,7 +630,7 @@ int32_t swattn_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
     return SWATTN_EUNSUPPORTED;
   }
   return launch_sparse_bwd(cfg, Q, K, V, n, topk, topk_cnt, O, lse, dO, dQ, dK, dV, workspace,
-                           workspace_bytes, num_sms(), static_cast<cudaStream_t>(stream));
+                           workspace_bytes, num_sms(), 0, static_cast<cudaStream_t>(stream));
 }
 
 int32_t swattn_dense_fwd(const swattn_config *cfg, const void *Q, const void *K, const void *V,

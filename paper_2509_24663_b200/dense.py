@@ -73,3 +73,38 @@ def tiled_gqa_forward(Q, K, V, cfg: AttentionConfig, B_q: int = 64, B_k: int = 6
 
 
 naive_gqa_forward = tiled_gqa_forward  # same semantics (dense.py:64-109); one kernel serves both
+
+
+def naive_gqa_backward(Q, K, V, dO, cfg: AttentionConfig, causal: bool = True,
+                       counter: OpCounter | None = None):
+    """dense.py:173-221 on the GPU: gradients of sum(O * dO) w.r.t. Q, K, V for
+    (causal) GQA attention -- the sparse backward's kernels with every
+    (causal) block visible, after the K5 forward for O / lse.  dK / dV reduce
+    in a fixed order (bitwise reproducible, :182-183).  Returns (dQ, dK, dV)
+    in the storage dtype (device bf16 tensors, or numpy bf16 for host
+    inputs)."""
+    n, h_q, h_kv, d_h = check_gqa_shapes(Q, K, V, cfg)
+    if tuple(dO.shape) != tuple(Q.shape):
+        raise ValueError(f"dO shape {tuple(dO.shape)} != Q shape {tuple(Q.shape)}")
+    host = is_host(Q)
+    Qd, Kd, Vd, dOd = (to_device_bf16(x, nm) for x, nm in ((Q, "Q"), (K, "K"), (V, "V"),
+                                                          (dO, "dO")))
+    fwd = tiled_gqa_forward(Qd, Kd, Vd, cfg, causal=causal)
+    dQ, dK, dV = torch.empty_like(Qd), torch.empty_like(Kd), torch.empty_like(Vd)
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+    ws = torch.empty(max(L.swattn_dense_bwd_workspace_bytes(c, n, int(bool(causal))), 1),
+                     dtype=torch.uint8, device=Qd.device)
+    _lib.check(L.swattn_dense_bwd(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), n,
+                                  int(bool(causal)), fwd.output.data_ptr(), fwd.lse.data_ptr(),
+                                  dOd.data_ptr(), dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), _lib.stream_handle(Qd.device)),
+               "swattn_dense_bwd")
+    if counter is not None:
+        vis = n * (n + 1) // 2 if causal else n * n
+        counter.add(mac=4 * vis * d_h * h_q, exp=vis * h_q)
+    if host:
+        import ml_dtypes
+        return tuple(t.cpu().view(torch.int16).numpy().view(ml_dtypes.bfloat16)
+                     for t in (dQ, dK, dV))
+    return dQ, dK, dV

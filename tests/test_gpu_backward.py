@@ -84,3 +84,27 @@ def test_backward_errors():
     sel = select_blocks(Qd, Kd, cfg, mode="approx")
     with pytest.raises(ValueError):
         sparse_backward(Qd, Kd, Vd, sel, _dev(dO)[:64], cfg)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_dense_backward(causal):
+    """naive_gqa_backward (dense.py:173-221) vs the reference's own gradients
+    (golden, causal) and the float64 oracle (non-causal), deterministic."""
+    from paper_2509_24663_b200.dense import naive_gqa_backward
+    rec = load_golden("bwd_dense_paper_n200_s4")
+    n = int(rec["n"])
+    Q, K, V, dO = _inputs(n, int(rec["seed"]))
+    assert O.digest(Q, K, V) == str(rec["digest"])
+    cfg = AttentionConfig()
+    Qd, Kd, Vd, dOd = _dev(Q), _dev(K), _dev(V), _dev(dO)
+    dQ, dK, dV = naive_gqa_backward(Qd, Kd, Vd, dOd, cfg, causal=causal)
+    if causal:
+        bf = lambda b: b.view(ml_dtypes.bfloat16).astype(np.float64)
+        want = (bf(rec["dbwd_dQ_bits"]), bf(rec["dbwd_dK_bits"]), bf(rec["dbwd_dV_bits"]))
+    else:
+        want = O.dense_backward(Q, K, V, dO, O.PAPER, causal=False)
+    for got, w, nm in zip((dQ, dK, dV), want, ("dQ", "dK", "dV")):
+        _close(_f64(got), w, nm)
+    again = naive_gqa_backward(Qd, Kd, Vd, dOd, cfg, causal=causal)
+    for a, b in zip((dQ, dK, dV), again):
+        assert torch.equal(a, b)

@@ -110,7 +110,7 @@ def test_spec_known_answers():
     assert O.sparse_visible_tokens(32767, cfg) == 6144
 
 
-@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith("bwd_")])
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith("bwd_") and "dense" not in n])
 def test_backward_matches_reference(name):
     """sparse_backward (sparse.py:130-185) with dO = make_qkv(seed + 1000).Q:
     dQ on the stored rows; dK / dV on the stored key rows when the oracle can
@@ -130,3 +130,16 @@ def test_backward_matches_reference(name):
         kr = rec["bwd_key_rows"]
         _bf16_close(dK[kr], rec["bwd_dK_bits"])
         _bf16_close(dV[kr], rec["bwd_dV_bits"])
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith("bwd_dense")])
+def test_dense_backward_matches_reference(name):
+    """naive_gqa_backward (dense.py:173-221), dO = make_qkv(seed + 1000).Q."""
+    rec = load_golden(name)
+    cfg, Q, K, V = _inputs(rec)
+    n = int(rec["n"])
+    dO, _, _ = O.draw_qkv(n, cfg.h_q, cfg.h_kv, cfg.d_h, int(rec["seed"]) + 1000)
+    dQ, dK, dV = O.dense_backward(Q, K, V, dO, cfg)
+    _bf16_close(dQ, rec["dbwd_dQ_bits"])
+    _bf16_close(dK, rec["dbwd_dK_bits"])
+    _bf16_close(dV, rec["dbwd_dV_bits"])
