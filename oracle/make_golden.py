@@ -131,6 +131,16 @@ def main():
             rec["dbwd_dQ_bits"] = _bits(dQ)
             rec["dbwd_dK_bits"] = _bits(dK)
             rec["dbwd_dV_bits"] = _bits(dV)
+        if name == "paper_n300_s5":
+            # the reference's own file writers (core.py:258-275, selection.py:386-400)
+            import tempfile
+            from swattn.core import save_tensor
+            from swattn.selection import save_selection
+            with tempfile.TemporaryDirectory() as d:
+                save_selection(sel, os.path.join(d, "s.bin"))
+                save_tensor(np.asarray(rec["sparse_lse"], dtype=np.float64), os.path.join(d, "t.swt"))
+                rec["selection_file"] = np.frombuffer(open(os.path.join(d, "s.bin"), "rb").read(), np.uint8)
+                rec["tensor_file"] = np.frombuffer(open(os.path.join(d, "t.swt"), "rb").read(), np.uint8)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **rec)
         print(f"{name}: {time.time() - t0:.1f}s -> {os.path.getsize(path) / 1e6:.2f} MB",

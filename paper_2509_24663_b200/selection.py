@@ -234,3 +234,100 @@ def fused_shared_scores_approx(Q, ck1: CompressedKeys, ck2: CompressedKeys, cfg:
     if B_q < 1 or B_k < 1:
         raise ValueError(f"tile sizes must be >= 1, got B_q={B_q}, B_k={B_k}")
     return _shared(Q, ck1, ck2, cfg, 2)
+
+
+# ---------------------------------------------------------------- selection fixtures
+SELECTION_TAG = 0xB5  # selection.py:48
+
+
+def _full_block_lists(sel: BlockSelection):
+    """Flat u32 stream of the reference fixture body: per (group, row) the
+    count then the ascending block ids (init below lo, top-k, local [lo, b]),
+    built vectorised from the device top-k lists."""
+    top, cnt = sel._host_topk()
+    G, n = cnt.shape
+    B = sel.block_size
+    i = np.arange(n, dtype=np.int64)
+    b = i // B
+    lo = np.maximum(0, b - sel.N_local + 1)
+    ninit = np.minimum(sel.N_init, lo)                      # init blocks below lo
+    nloc = b - lo + 1
+    sizes = ninit[None, :] + cnt.astype(np.int64) + nloc[None, :]   # [G, n]
+    row_len = 1 + sizes.ravel()
+    starts = np.concatenate([[0], np.cumsum(row_len)[:-1]])
+    out = np.empty(int(row_len.sum()), dtype="<u4")
+    out[starts] = sizes.ravel()
+    # position of each entry inside its row, then its block id
+    total_entries = int(sizes.sum())
+    row_of = np.repeat(np.arange(G * n), sizes.ravel())
+    first = np.repeat(starts + 1, sizes.ravel())
+    k = np.arange(total_entries) - np.repeat(np.cumsum(sizes.ravel()) - sizes.ravel(), sizes.ravel())
+    r_i = row_of % n
+    r_g = row_of // n
+    ni, ct = ninit[r_i], cnt.reshape(-1)[row_of].astype(np.int64)
+    ids = np.where(k < ni, k,
+                   np.where(k < ni + ct, top.reshape(G * n, -1)[row_of, np.clip(k - ni, 0, top.shape[2] - 1)],
+                            lo[r_i] + (k - ni - ct)))
+    del r_g
+    out[first + k] = ids.astype("<u4")
+    return out
+
+
+def save_selection(sel: BlockSelection, path) -> None:
+    """selection.py:386-400: core magic, tag byte, u32 groups / n / block
+    size, then per (group, row) a u32 count and that many u32 block ids."""
+    import struct
+
+    from .core import TENSOR_MAGIC, atomic_write_bytes
+    head = TENSOR_MAGIC + struct.pack("<B", SELECTION_TAG) + struct.pack(
+        "<III", sel.num_groups, sel.n, sel.block_size)
+    atomic_write_bytes(path, head + _full_block_lists(sel).tobytes())
+
+
+def load_selection(path, N_init: int = 1, N_local: int = 32, device=None) -> BlockSelection:
+    """selection.py:403-430 with the same errors.  The fixture stores full
+    block sets; the init (N_init) / local (N_local) structure -- not in the
+    file, paper defaults -- is split off so the result is a device
+    BlockSelection (top-k lists) ready for sparse_forward."""
+    import struct
+
+    from .core import TENSOR_MAGIC, TensorFormatError
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    head = len(TENSOR_MAGIC)
+    if len(blob) < head + 13 or blob[:head] != TENSOR_MAGIC:
+        raise TensorFormatError(f"malformed header: bad magic in {path}")
+    (tag,) = struct.unpack_from("<B", blob, head)
+    if tag != SELECTION_TAG:
+        raise TensorFormatError(f"not a selection fixture: tag {tag}")
+    groups, n, block_size = struct.unpack_from("<III", blob, head + 1)
+    body = np.frombuffer(blob, dtype="<u4", offset=head + 13) if len(blob) > head + 13 else \
+        np.empty(0, dtype="<u4")
+    rows, off = [], 0
+    for _ in range(groups * n):
+        if off >= body.size:
+            raise TensorFormatError("truncated payload: row count missing")
+        c = int(body[off])
+        if off + 1 + c > body.size:
+            raise TensorFormatError("truncated payload: row indices missing")
+        rows.append(body[off + 1: off + 1 + c].astype(np.int64))
+        off += 1 + c
+    if off != body.size:
+        raise TensorFormatError("oversized payload: trailing bytes")
+    k_top = 0
+    tops = []
+    for r, blocks in enumerate(rows):
+        i = r % n
+        b = i // block_size
+        lo = max(0, b - N_local + 1)
+        t = blocks[(blocks >= N_init) & (blocks < lo)]
+        tops.append(t)
+        k_top = max(k_top, t.size)
+    top = np.full((groups, n, max(k_top, 1)), -1, dtype=np.int32)
+    cnt = np.zeros((groups, n), dtype=np.int32)
+    for r, t in enumerate(tops):
+        top[r // n, r % n, :t.size] = t
+        cnt[r // n, r % n] = t.size
+    dev = device or ("cuda" if torch.cuda.is_available() else "cpu")
+    return BlockSelection(block_size, n, torch.from_numpy(top).to(dev), torch.from_numpy(cnt).to(dev),
+                          N_init, N_local)
