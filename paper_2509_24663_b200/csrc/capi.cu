@@ -114,7 +114,8 @@ static SelectLayout select_layout(const swattn_config *cfg, int64_t n) {
   L.off_scmp = o; o = align_up(o + (size_t)cfg->h_kv * n * L.ld * 4);
   L.off_flags = o; o = align_up(o + (size_t)cfg->h_kv * n * L.ld_f * 8);
   L.off_count = o; o = align_up(o + 16);
-  L.off_rows = o; o = align_up(o + (size_t)cfg->h_kv * n * 4);
+  // flagged row ids [cap] followed by their k-th keys [cap] (K3 -> re-rank)
+  L.off_rows = o; o = align_up(o + (size_t)cfg->h_kv * n * 4 * 2);
   L.off_part = o; o = align_up(o + rerank_partials_bytes());
   L.off_shared = o;
   if (L.generic) o = align_up(o + (size_t)n * cfg->h_kv * L.m1 * 4);

@@ -168,10 +168,23 @@ __global__ void __launch_bounds__(256) decode_pass1_kernel(DecodeArgs a, float2 
 }
 
 // ------------------------------------------------------------ D3 pass 2
-// grid (batch*h_kv, tiles), 128 threads: thread = C1 column of the tile.
-__global__ void __launch_bounds__(128, 4) decode_pass2_kernel(DecodeArgs a, const float2 *part,
+// grid (batch*h_kv, tiles), 4 warps: warp w scores columns [32 w, 32 w + 32)
+// of the 128-column tile on the tensor cores -- S [16 heads x 32 columns] =
+// q (A fragments, registers) . K_C1 rows (B fragments straight from global
+// memory) with mma.sync.m16n8k16 -- then p = exp2(s c - m_h) / l_h summed over
+// the 16 heads (two rows per thread + three shuffles), 5/4 max-pool from
+// shared memory (compression.py:160-173).
+__device__ __forceinline__ void mma16816_dec(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                             uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const float2 *part,
                                                            int splits, float *s_cmp, int64_t ld) {
-  __shared__ __align__(16) float q_s[kG][kD];
   __shared__ float2 stat[kG];  // (m, 1/l), log2 domain
   __shared__ float sc[kTileCols + 4];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
@@ -183,8 +196,7 @@ __global__ void __launch_bounds__(128, 4) decode_pass2_kernel(DecodeArgs a, cons
   const int t = blockIdx.y;
   if (t * kTileBlocks >= hi) return;
   const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
-  for (int e = threadIdx.x; e < kG * kD; e += blockDim.x)
-    q_s[e / kD][e % kD] = bf2f(a.q[((int64_t)seq * a.h_q + g * kG) * kD + e]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < kG) {
     const int h = threadIdx.x;
     float M = -INFINITY;
@@ -196,22 +208,58 @@ __global__ void __launch_bounds__(128, 4) decode_pass2_kernel(DecodeArgs a, cons
     }
     stat[h] = make_float2(M == -INFINITY ? 0.f : M, S > 0.f ? 1.f / S : 0.f);
   }
-  __syncthreads();
-  const int64_t col = (int64_t)t * kTileBlocks * kPoolS + threadIdx.x;
-  float v = -INFINITY;
-  if (col < m1) {
-    v = 0.f;
-    if (col < vis1) {
-      float sv[kG];
-      logits16(q_s, a.kc1 + (((int64_t)seq * a.max_m1 + col) * a.h_kv + g) * kD, sv);
-      float acc = 0.f;
+  // q as A fragments: a0 = (head r, d k), a1 = (r + 8, k), a2 = (r, k + 8), a3 = (r + 8, k + 8)
+  const int r = lane >> 2, dw = lane & 3;
+  const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.q + (((int64_t)seq * a.h_q + g * kG + r) * kD));
+  const uint32_t *q1 = q0 + 8 * (kD / 2);
+  uint32_t qa[8][4];
 #pragma unroll
-      for (int h = 0; h < kG; ++h)
-        acc = fmaf(fast_exp2(sv[h] * a.scale_log2 - stat[h].x), stat[h].y, acc);
-      v = acc;
+  for (int ks = 0; ks < 8; ++ks) {
+    qa[ks][0] = __ldg(q0 + ks * 8 + dw);
+    qa[ks][1] = __ldg(q1 + ks * 8 + dw);
+    qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
+    qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
+  }
+  // B fragments: column (n) = lane / 4 of each 8-column n-tile, d = 16 ks + 2 (lane % 4)
+  const int64_t col0 = (int64_t)t * kTileBlocks * kPoolS + warp * 32;
+  const __nv_bfloat16 *kbase = a.kc1 + ((int64_t)seq * a.max_m1 * a.h_kv + g) * kD;
+  float acc[4][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+    const int64_t col = col0 + nt * 8 + r;
+    const bool ok = col < vis1;  // invisible / missing columns are masked below
+    const uint32_t *kr = reinterpret_cast<const uint32_t *>(kbase + (ok ? col : 0) * a.h_kv * kD);
+    uint32_t kb[8][2];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      kb[ks][0] = ok ? __ldg(kr + ks * 8 + dw) : 0u;
+      kb[ks][1] = ok ? __ldg(kr + ks * 8 + 4 + dw) : 0u;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) mma16816_dec(acc[nt], qa[ks], kb[ks][0], kb[ks][1]);
+  }
+  __syncthreads();  // stat
+  const float2 st0 = stat[r], st1 = stat[r + 8];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    // rows r (c0, c1) and r + 8 (c2, c3); columns 2 (lane % 4) + {0, 1}
+    float c0 = fast_exp2(fmaf(acc[nt][0], a.scale_log2, -st0.x)) * st0.y +
+               fast_exp2(fmaf(acc[nt][2], a.scale_log2, -st1.x)) * st1.y;
+    float c1 = fast_exp2(fmaf(acc[nt][1], a.scale_log2, -st0.x)) * st0.y +
+               fast_exp2(fmaf(acc[nt][3], a.scale_log2, -st1.x)) * st1.y;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    }
+    if (r == 0) {
+      const int cc = warp * 32 + nt * 8 + 2 * dw;
+      const int64_t col = col0 + nt * 8 + 2 * dw;
+      sc[cc] = col < m1 ? (col < vis1 ? c0 : 0.f) : -INFINITY;
+      sc[cc + 1] = col + 1 < m1 ? (col + 1 < vis1 ? c1 : 0.f) : -INFINITY;
     }
   }
-  sc[threadIdx.x] = v;
   __syncthreads();
   if (threadIdx.x < kTileBlocks) {
     const int j = t * kTileBlocks + threadIdx.x;
@@ -514,7 +562,7 @@ static DecodeLayout decode_layout(const swattn_config *cfg, int batch, int max_p
   D.off_topk = o; o = al(o + rows * std::max(cfg->k_top, 1) * sizeof(int32_t));
   D.off_cnt = o; o = al(o + rows * sizeof(int32_t));
   D.off_count = o; o = al(o + 16);
-  D.off_rows = o; o = al(o + rows * sizeof(int32_t));
+  D.off_rows = o; o = al(o + 2 * rows * sizeof(int32_t));  // row ids + k-th keys
   D.off_part = o; o = al(o + rerank_partials_bytes());
   D.off_po = o; o = al(o + rows * D.attn_splits * kG * kD * sizeof(float));
   D.off_pml = o; o = al(o + rows * D.attn_splits * kG * sizeof(float2));

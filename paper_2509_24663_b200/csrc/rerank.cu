@@ -196,31 +196,11 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_p1_kernel(RerankArgs a) {
   }
 }
 
-__device__ double block_reduce_max(double v, double *red) {
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  v = -INFINITY;
-  for (int w = 0; w < kThreads / 32; ++w) v = fmax(v, red[w]);
-  return v;
-}
-__device__ double block_reduce_sum(double v, double *red) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  v = 0.0;
-  for (int w = 0; w < kThreads / 32; ++w) v += red[w];
-  return v;
-}
-
 __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
   __shared__ __align__(16) double q_s[kD][kG];
   __shared__ double lse_s[kG];
   __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
   extern __shared__ __nv_bfloat16 kc_s[];  // [kD][kChunk]
-  __shared__ double red[kThreads / 32];
   __shared__ int members[kMaxCluster];
   __shared__ double mscore[kMaxCluster];
   __shared__ int n_members, n_above;
@@ -269,15 +249,8 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
 
     // ---- the boundary cluster from the float32 scores
     const float *src = a.s_cmp + (int64_t)row * a.ld;
-    // k-th largest float32 score (same order as K3)
-    uint32_t T = 0;
-    for (int bit = 31; bit >= 0; --bit) {
-      const uint32_t candk = T | (1u << bit);
-      int c = 0;
-      for (int t = threadIdx.x; t < ncand; t += kThreads) c += f2key(src[a.N_init + t]) >= candk;
-      c = (int)block_reduce_sum((double)c, red);
-      if (c >= k) T = candk;
-    }
+    // k-th largest float32 score key, recorded by K3 next to the row id
+    const uint32_t T = (uint32_t)a.rows[a.cap + item];
     const float vk = key2f(T);
     const float band = 3.0f * kScoreRelErr * fabsf(vk);
     if (threadIdx.x == 0) { n_members = 0; n_above = 0; }

@@ -27,7 +27,7 @@ constexpr int kMaxCand = 4096;  // per-row candidate bound held in smem
 
 struct AmbList {
   int32_t *count;         // device counter
-  int32_t *rows;          // [cap] row ids
+  int32_t *rows;          // [cap] row ids, then [cap] k-th keys (the re-rank's T)
   int32_t cap;
   const uint64_t *flags;  // [rows, ld_f] or null
   int64_t ld_f;
@@ -179,7 +179,10 @@ __device__ void warp_topk_generic(const Keys ks, int ncand, int k, int N_init, i
   }
   if (ambiguous && lane == 0) {
     const int slot = atomicAdd(amb.count, 1);
-    if (slot < amb.cap) amb.rows[slot] = (int32_t)row;
+    if (slot < amb.cap) {
+      amb.rows[slot] = (int32_t)row;
+      amb.rows[amb.cap + slot] = (int32_t)T;
+    }
   }
 }
 
@@ -463,7 +466,10 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
   }
   if (ambiguous && lane == 0) {
     const int slot = atomicAdd(amb.count, 1);
-    if (slot < amb.cap) amb.rows[slot] = (int32_t)row;
+    if (slot < amb.cap) {
+      amb.rows[slot] = (int32_t)row;
+      amb.rows[amb.cap + slot] = (int32_t)T;
+    }
   }
 }
 
