@@ -36,11 +36,10 @@ size_t rerank_partials_bytes();
 
 namespace {
 
-constexpr int kP1Cols = 256;     // C2 columns per pass-1 CTA
+constexpr int kP1Cols = 128;     // normaliser columns per pass-1 CTA (4 warps x 32)
 constexpr int kTileBlocks = 31;  // pass-2 tile: 31 blocks, 124 (+4) columns
 constexpr int kTileCols = 128;
 constexpr int kAttnBlocks = 4;   // visible blocks per split-KV warp (24 splits at batch 16)
-constexpr int kMaxSplits = 16;
 
 struct DecodeArgs {
   const __nv_bfloat16 *q;            // [batch][h_q][d]
@@ -60,41 +59,6 @@ __device__ __forceinline__ const __nv_bfloat16 *page_row(const __nv_bfloat16 *pa
                                                          int64_t token, int h_kv, int g) {
   const int page = bt[(int64_t)seq * max_pages + token / kB];
   return pages + (((int64_t)page * kB + token % kB) * h_kv + g) * kD;
-}
-
-// the 16 head logits of one row, the row streamed in two 64-element halves
-// (8 x 16 B loads in flight, ~80 registers: several CTAs per SM)
-__device__ __forceinline__ void logits16(const float (*q_s)[kD], const __nv_bfloat16 *k, float (&s)[kG]) {
-#pragma unroll
-  for (int h = 0; h < kG; ++h) s[h] = 0.f;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    uint4 kr[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) kr[i] = __ldg(reinterpret_cast<const uint4 *>(k + half * 64) + i);
-#pragma unroll
-    for (int h = 0; h < kG; ++h) {
-      const float *q = q_s[h] + half * 64;
-      float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const __nv_bfloat162 *v = reinterpret_cast<const __nv_bfloat162 *>(&kr[i]);
-        const float4 qa = *reinterpret_cast<const float4 *>(q + 8 * i);
-        const float4 qb = *reinterpret_cast<const float4 *>(q + 8 * i + 4);
-        const float2 f0 = __bfloat1622float2(v[0]), f1 = __bfloat1622float2(v[1]);
-        const float2 f2 = __bfloat1622float2(v[2]), f3 = __bfloat1622float2(v[3]);
-        a0 = fmaf(qa.x, f0.x, a0);
-        a1 = fmaf(qa.y, f0.y, a1);
-        a0 = fmaf(qa.z, f1.x, a0);
-        a1 = fmaf(qa.w, f1.y, a1);
-        a0 = fmaf(qb.x, f2.x, a0);
-        a1 = fmaf(qb.y, f2.y, a1);
-        a0 = fmaf(qb.z, f3.x, a0);
-        a1 = fmaf(qb.w, f3.y, a1);
-      }
-      s[h] += a0 + a1;
-    }
-  }
 }
 
 // ------------------------------------------------------------ D1 append
@@ -119,50 +83,91 @@ __global__ void kcache_append_kernel(DecodeArgs a, const int32_t *prev_lens) {
 }
 
 // ------------------------------------------------------------ D2 pass 1
-// grid (batch*h_kv, splits), 256 threads: thread = C2 column, 16 heads each.
-__global__ void __launch_bounds__(256) decode_pass1_kernel(DecodeArgs a, float2 *part, int splits) {
-  __shared__ __align__(16) float q_s[kG][kD];
-  __shared__ float2 red[8][kG];
+// grid (batch*h_kv, splits), 4 warps: warp w scores normaliser columns
+// [128 split + 32 w, +32) on mma.sync (q as A fragments, key rows as B
+// fragments from global memory) and keeps per-head online (max, sum); the
+// four lanes sharing a head row, then the four warps, are merged.
+__device__ __forceinline__ void merge_ml(float &m, float &l, float m2, float l2) {
+  const float M = fmaxf(m, m2);
+  if (M == -INFINITY) return;
+  l = (m == -INFINITY ? 0.f : l * fast_exp2(m - M)) + (m2 == -INFINITY ? 0.f : l2 * fast_exp2(m2 - M));
+  m = M;
+}
+
+__device__ __forceinline__ void mma16816_p1(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                            uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(128) decode_pass1_kernel(DecodeArgs a, float2 *part, int splits) {
+  __shared__ float2 red[4][kG];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
   const int64_t vis2 = vis_count(L - 1, a.l_C2, a.s_C2);
   const int64_t vis1 = vis_count(L - 1, a.l_C1, a.s_C1);
   const bool use2 = vis2 > 0;
   const int64_t vis = use2 ? vis2 : vis1;  // fallback rows use the exact C1 lse
-  const __nv_bfloat16 *kc = (use2 ? a.kc2 : a.kc1) + (int64_t)seq * (use2 ? a.max_m2 : a.max_m1) * a.h_kv * kD;
-  for (int t = threadIdx.x; t < kG * kD; t += blockDim.x)
-    q_s[t / kD][t % kD] = bf2f(a.q[((int64_t)seq * a.h_q + g * kG) * kD + t]);
-  __syncthreads();
-  float m[kG], l[kG];
+  const __nv_bfloat16 *kc = (use2 ? a.kc2 : a.kc1) + ((int64_t)seq * (use2 ? a.max_m2 : a.max_m1) * a.h_kv + g) * kD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, dw = lane & 3;
+  const int64_t col0 = (int64_t)blockIdx.y * 128 + warp * 32;
+  float m0 = -INFINITY, l0 = 0.f, m1 = -INFINITY, l1 = 0.f;  // heads r, r + 8
+  if (col0 < vis) {
+    const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.q + (((int64_t)seq * a.h_q + g * kG + r) * kD));
+    const uint32_t *q1 = q0 + 8 * (kD / 2);
+    uint32_t qa[8][4];
 #pragma unroll
-  for (int h = 0; h < kG; ++h) { m[h] = -INFINITY; l[h] = 0.f; }
-  const int64_t c = (int64_t)blockIdx.y * kP1Cols + threadIdx.x;
-  if (c < vis) {
-    float sv[kG];
-    logits16(q_s, kc + (c * a.h_kv + g) * kD, sv);
+    for (int ks = 0; ks < 8; ++ks) {
+      qa[ks][0] = __ldg(q0 + ks * 8 + dw);
+      qa[ks][1] = __ldg(q1 + ks * 8 + dw);
+      qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
+      qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
+    }
 #pragma unroll
-    for (int h = 0; h < kG; ++h) {
-      m[h] = sv[h] * a.scale_log2;
-      l[h] = 1.f;
+    for (int nt = 0; nt < 4; ++nt) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int64_t col = col0 + nt * 8 + r;
+      const bool ok = col < vis;
+      const uint32_t *kr = reinterpret_cast<const uint32_t *>(kc + (ok ? col : 0) * a.h_kv * kD);
+      uint32_t kb[8][2];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        kb[ks][0] = ok ? __ldg(kr + ks * 8 + dw) : 0u;
+        kb[ks][1] = ok ? __ldg(kr + ks * 8 + 4 + dw) : 0u;
+      }
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) mma16816_p1(acc, qa[ks], kb[ks][0], kb[ks][1]);
+      // columns 2 dw, 2 dw + 1 of this n-tile
+      const int64_t c = col0 + nt * 8 + 2 * dw;
+      const bool v0 = c < vis, v1 = c + 1 < vis;
+      const float x0 = v0 ? acc[0] * a.scale_log2 : -INFINITY, x1 = v1 ? acc[1] * a.scale_log2 : -INFINITY;
+      const float x2 = v0 ? acc[2] * a.scale_log2 : -INFINITY, x3 = v1 ? acc[3] * a.scale_log2 : -INFINITY;
+      const float mm0 = fmaxf(x0, x1), mm1 = fmaxf(x2, x3);
+      if (mm0 != -INFINITY) merge_ml(m0, l0, mm0, fast_exp2(x0 - mm0) + fast_exp2(x1 - mm0));
+      if (mm1 != -INFINITY) merge_ml(m1, l1, mm1, fast_exp2(x2 - mm1) + fast_exp2(x3 - mm1));
     }
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // lanes 4 r .. 4 r + 3 share head rows r and r + 8
 #pragma unroll
-  for (int h = 0; h < kG; ++h) {
-    float M = m[h];
-    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float S = (m[h] == -INFINITY) ? 0.f : l[h] * fast_exp2(m[h] - M);
-    for (int o = 16; o; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
-    if (lane == 0) red[warp][h] = make_float2(M, S);
+  for (int o = 1; o < 4; o <<= 1) {
+    const float om0 = __shfl_xor_sync(0xffffffffu, m0, o), ol0 = __shfl_xor_sync(0xffffffffu, l0, o);
+    const float om1 = __shfl_xor_sync(0xffffffffu, m1, o), ol1 = __shfl_xor_sync(0xffffffffu, l1, o);
+    merge_ml(m0, l0, om0, ol0);
+    merge_ml(m1, l1, om1, ol1);
+  }
+  if (dw == 0) {
+    red[warp][r] = make_float2(m0, l0);
+    red[warp][r + 8] = make_float2(m1, l1);
   }
   __syncthreads();
   if (threadIdx.x < kG) {
     const int h = threadIdx.x;
-    float M = -INFINITY;
-    for (int w = 0; w < 8; ++w) M = fmaxf(M, red[w][h].x);
-    float S = 0.f;
-    for (int w = 0; w < 8; ++w)
-      if (red[w][h].x != -INFINITY) S += red[w][h].y * fast_exp2(red[w][h].x - M);
+    float M = -INFINITY, S = 0.f;
+    for (int w = 0; w < 4; ++w) merge_ml(M, S, red[w][h].x, red[w][h].y);
     part[((int64_t)row * splits + blockIdx.y) * kG + h] = make_float2(M, S);
   }
 }
@@ -651,7 +656,7 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
   float2 *pml = reinterpret_cast<float2 *>(ws + D.off_pml);
   DecodeArgs a = make_args(cfg, kv, q, batch);
   const int nrows = batch * cfg->h_kv;
-  decode_pass1_kernel<<<dim3(nrows, D.p1_splits), 256, 0, st>>>(a, p1, D.p1_splits);
+  decode_pass1_kernel<<<dim3(nrows, D.p1_splits), 128, 0, st>>>(a, p1, D.p1_splits);
   SWATTN_LAUNCH_CHECK("decode_pass1_kernel");
   decode_pass2_kernel<<<dim3(nrows, D.tiles), 128, 0, st>>>(a, p1, D.p1_splits, scmp, D.ld);
   SWATTN_LAUNCH_CHECK("decode_pass2_kernel");

@@ -525,12 +525,23 @@ decode_topk_kernel(const float *__restrict__ s_cmp, int64_t ld, const int32_t *_
   const int ncand = hi > N_init ? hi - N_init : 0;
   const int k = (i + 1) < l_C1 ? 0 : min(ncand, k_top);
   if (lane == 0) topk_cnt[row] = k;
-  if (kReg)
+  if (kReg && n_cols <= kRegSpan) {
     warp_topk_row_reg(s_cmp + row * ld, (int)ld, ncand, k, N_init, k_top, topk + row * k_top,
                       reg_s[kReg ? warp : 0], hist_s + warp * 256, amb, row);
-  else
+  } else if (kReg) {
+    // this sequence is longer than the register path covers: generic path
+    // straight from S^cmp (the kernel was launched without a staging buffer)
+    int32_t *out = topk + row * k_top;
+    if (k == ncand) {
+      for (int t = lane; t < k_top; t += 32) out[t] = t < k ? N_init + t : -1;
+    } else {
+      warp_topk_generic(GlobalKeys{s_cmp + row * ld + N_init}, ncand, k, N_init, k_top, out,
+                        hist_s + warp * 256, amb, row);
+    }
+  } else {
     warp_topk_row(s_cmp + row * ld + N_init, ncand, k, N_init, k_top, topk + row * k_top,
                   keys_s + (size_t)warp * cand_stride, hist_s + warp * 256, amb, row);
+  }
 }
 
 bool reg_path_ok(const float *s_cmp, int64_t ld, int k_top, int n_cols) {
@@ -586,7 +597,8 @@ int32_t launch_decode_topk(const swattn_config *cfg, const float *s_cmp, int64_t
   AmbList amb{amb_count, amb_rows, amb_cap, nullptr, 0};
   const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
   const unsigned grid = (unsigned)cdiv(rows, kWarps);
-  if (reg_path_ok(s_cmp, ld, cfg->k_top, n_cols)) {
+  // rows decide per sequence length; the register path needs only alignment here
+  if (reg_path_ok(s_cmp, ld, cfg->k_top, 0)) {
     decode_topk_kernel<true><<<grid, kWarps * 32, 0, stream>>>(
         s_cmp, ld, seq_lens, batch, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top,
         cfg->l_C1, cfg->s_C1, cfg->s, cand_stride, topk, topk_cnt, amb);
