@@ -296,6 +296,21 @@ def run_ours(args):
                          "peak_source": f"{peaks['source']} "
                                         f"({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})"},
             "stages_ms": stages,
+            "roofline_parts": {
+                "K4_part_A_fa_tile (tcgen05, init+local blocks)": {
+                    "ms": stages["K4_part_A_fa_tile"], "bound": "tensor", "unit": "TFLOP/s",
+                    "achieved": part_a_flop(cfg, n) / (stages["K4_part_A_fa_tile"] / 1e3) / 1e12,
+                    "peak": peaks["tflops_sustained"],
+                    "frac": part_a_flop(cfg, n) / (stages["K4_part_A_fa_tile"] / 1e3) / 1e12
+                    / peaks["tflops_sustained"]},
+                "K4_part_B_sparse_pw (mma.sync, per-token top-k gather)": {
+                    "ms": stages["K4_part_B_sparse_pw_est"], "bound": "L2->SM gather",
+                    "unit": "TB/s",
+                    "achieved": _gather_bytes(cfg, n) / (stages["K4_part_B_sparse_pw_est"] / 1e3) / 1e12,
+                    "peak": 19.7,
+                    "frac": _gather_bytes(cfg, n) / (stages["K4_part_B_sparse_pw_est"] / 1e3) / 1e12 / 19.7,
+                    "peak_source": "per-SM gather ceiling 133 GB/s x 148 (profiles/r01c_gather_sm_sweep.txt)"},
+            },
             "k4_gather": {"bytes": _gather_bytes(cfg, n),
                           "achieved_TBs_over_K4": _gather_bytes(cfg, n) / (stages["K4_sparse_attention"] / 1e3) / 1e12,
                           "l2_gather_peak_TBs": 19.7,
@@ -383,6 +398,15 @@ def stage_breakdown(L, c, cfg, Q, K, V, n, stream, reps=2):
                                                            lse.data_ptr(), work.data_ptr(), wsb,
                                                            sh),
     }
+    # part A alone (init + local blocks on the tcgen05 FA tile): the same call
+    # with k_top = 0 skips part B (selection.py:123 picks nothing)
+    import dataclasses
+    c0 = _lib.c_config(dataclasses.replace(cfg, k_top=0))
+    calls["K4_part_A_fa_tile"] = lambda: L.swattn_sparse_fwd(c0, Q.data_ptr(), K.data_ptr(),
+                                                             V.data_ptr(), n, topk.data_ptr(),
+                                                             cnt.data_ptr(), O_.data_ptr(),
+                                                             lse.data_ptr(), work.data_ptr(), wsb,
+                                                             sh)
     out = {}
     for name, fn in calls.items():
         _lib.check(fn(), name)
@@ -395,7 +419,18 @@ def stage_breakdown(L, c, cfg, Q, K, V, n, stream, reps=2):
         out[name] = a.elapsed_time(b) / reps
     out["rerank_est"] = max(0.0, out["select_total"] - out["K1_compress"] - out["K2_block_scores"]
                             - out["K3_topk"])
+    out["K4_part_B_sparse_pw_est"] = max(0.0, out["K4_sparse_attention"] - out["K4_part_A_fa_tile"])
     return out
+
+
+def part_a_flop(cfg, n):
+    """Algorithmic FLOPs of K4 part A: every token's init + local keys
+    (bench.py:139-141 restricted to the N_init + N_local blocks)."""
+    i = np.arange(n, dtype=np.int64)
+    b = i // cfg.B
+    picked = np.minimum(b + 1, cfg.N_init + cfg.N_local)
+    vis = int(((picked - 1) * cfg.B + (i - b * cfg.B) + 1).sum())
+    return 4 * cfg.h_q * vis * cfg.d_h
 
 
 def dense_comparator(Q, K, V, cfg, n, stream, reps=3):

@@ -401,10 +401,12 @@ struct DkvParams {
 };
 
 constexpr int kKvWarps = 4;  // 16 keys each
+constexpr int kKvBuf = 4;    // queries in flight (cp.async prefetch depth): the
+                             // L2 -> smem latency exceeds one query's compute
 struct __align__(128) DkvSmem {
-  uint8_t q[2][kG * kD * 2];   // 4 KB each, [head][d] swizzled (swz256)
-  uint8_t go[2][kG * kD * 2];
-  float lse[2][kG], delta[2][kG];
+  uint8_t q[kKvBuf][kG * kD * 2];   // 4 KB each, [head][d] swizzled (swz256)
+  uint8_t go[kKvBuf][kG * kD * 2];
+  float lse[kKvBuf][kG], delta[kKvBuf][kG];
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
@@ -447,16 +449,19 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
     }
     asm volatile("cp.async.commit_group;");
   };
-  if (npairs > 0) stage(0, 0);
+  // prologue: queries 0 .. kKvBuf-2 in flight (one commit group each, empty
+  // groups past the end keep the group count uniform)
+  for (int q = 0; q < kKvBuf - 1; ++q) {
+    if (q < npairs) stage(q, q);
+    else asm volatile("cp.async.commit_group;");
+  }
   const int lm = lane >> 3, lr = lane & 7;
   for (int64_t pi = 0; pi < npairs; ++pi) {
-    const int buf = (int)(pi & 1);
-    if (pi + 1 < npairs) {
-      stage(pi + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;");
-    } else {
-      asm volatile("cp.async.wait_group 0;");
-    }
+    const int buf = (int)(pi % kKvBuf);
+    const int64_t ahead = pi + kKvBuf - 1;
+    if (ahead < npairs) stage(ahead, (int)(ahead % kKvBuf));
+    else asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kKvBuf - 1));  // query pi has landed
     __syncthreads();
     const int64_t i = (int64_t)(p.keys[sg.begin + pi] & 0xffffffffull);
     const uint32_t qb = tc::smem_u32(sm.q[buf]), gb_ = tc::smem_u32(sm.go[buf]);
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
       mma16816(dk[2 * dpi], sa0, sa1, sa2, sa3, q00, q01);
       mma16816(dk[2 * dpi + 1], sa0, sa1, sa2, sa3, q10, q11);
     }
-    __syncthreads();  // buffer reuse by the stage two pairs ahead
+    __syncthreads();  // this buffer is refilled by the next iteration's prefetch
   }
   // partials: [seg][0 = dK, 1 = dV][64 keys][128 d]
   float *pk = p.part + (int64_t)seg_id * 2 * kBlk * kD;
