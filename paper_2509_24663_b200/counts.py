@@ -20,6 +20,28 @@ def sparse_visible_tokens(cfg: AttentionConfig, i: int) -> int:
     return (picked - 1) * cfg.B + (i - b * cfg.B) + 1
 
 
+def dense_query_counts(cfg: AttentionConfig, n: int):
+    """bench.py:103-104: (mac, exp) of the newest query at context n."""
+    return 2 * cfg.h_q * n * cfg.d_h, cfg.h_q * n
+
+
+def sparse_query_counts(cfg: AttentionConfig, n: int):
+    """bench.py:107-109."""
+    v = sparse_visible_tokens(cfg, n - 1)
+    return 2 * cfg.h_q * v * cfg.d_h, cfg.h_q * v
+
+
+def selection_query_counts(cfg: AttentionConfig, n: int, approx: bool) -> dict:
+    """bench.py:112-126: two-pass scoring cost of the newest query."""
+    v1 = pooled_visible_count(n - 1, cfg.l_C1, cfg.s_C1)
+    v2 = pooled_visible_count(n - 1, cfg.l_C2, cfg.s_C2)
+    pass1_cols = (v2 if v2 > 0 else v1) if approx else v1
+    pass1_mac = cfg.h_q * pass1_cols * cfg.d_h
+    pass2_mac = cfg.h_q * v1 * cfg.d_h
+    return {"mac": pass1_mac + pass2_mac, "exp": cfg.h_q * (pass1_cols + v1),
+            "pass1_mac": pass1_mac, "pass2_mac": pass2_mac}
+
+
 def _pooled_all(n: int, length: int, stride: int) -> np.ndarray:
     i = np.arange(n, dtype=np.int64)
     return np.where(i + 1 >= length, (i + 1 - length) // stride + 1, 0)
