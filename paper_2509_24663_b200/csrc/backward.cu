@@ -414,7 +414,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
 }
 
 __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_constant__ DkvParams p) {
-  __shared__ DkvSmem sm;
+  extern __shared__ __align__(128) uint8_t dkv_smem[];
+  DkvSmem &sm = *reinterpret_cast<DkvSmem *>(dkv_smem);
   const int seg_id = blockIdx.x;
   if (seg_id >= *p.n_segs) return;
   const Seg sg = p.segs[seg_id];
@@ -748,7 +749,13 @@ int32_t launch_sparse_bwd(const swattn_config *cfg, const void *Q, const void *K
     q.mode = mode;
     q.scale_log2 = scale * kLog2e;
     const int64_t max_segs = npairs / kSeg + L.n_gb + 1;
-    bwd_dkdv_kernel<<<(unsigned)max_segs, kKvWarps * 32, 0, st>>>(q);
+    static bool dkv_attr = false;
+    if (!dkv_attr) {
+      cudaFuncSetAttribute(bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(DkvSmem));
+      dkv_attr = true;
+    }
+    bwd_dkdv_kernel<<<(unsigned)max_segs, kKvWarps * 32, sizeof(DkvSmem), st>>>(q);
     SWATTN_LAUNCH_CHECK("bwd_dkdv_kernel");
     // B4
     bwd_reduce_kernel<<<(unsigned)L.n_gb, 256, 0, st>>>(n, L.nb, cfg->h_kv, seg_off, nseg, part, scale,
