@@ -70,6 +70,34 @@ def main():
         torch.cuda.synchronize()
         times.append(a.elapsed_time(b))
     ms = float(np.median(times))
+    # dense decode comparator: flash-attn 2.8 decode over the same 16 x 128K
+    # contexts held contiguously (its paged path needs 256-token pages)
+    dense = {}
+    try:
+        from flash_attn import flash_attn_with_kvcache
+        kc = torch.randn((B, L, cfg.h_kv, cfg.d_h), generator=g, device="cuda").to(torch.bfloat16)
+        vc = torch.randn((B, L, cfg.h_kv, cfg.d_h), generator=g, device="cuda").to(torch.bfloat16)
+        lens = torch.full((B,), L, dtype=torch.int32, device="cuda")
+        qd = q[:, None]
+
+        def dstep():
+            flash_attn_with_kvcache(qd, kc, vc, cache_seqlens=lens, causal=True)
+        dstep()
+        torch.cuda.synchronize()
+        dts = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dstep()
+            b.record(stream)
+            torch.cuda.synchronize()
+            dts.append(a.elapsed_time(b))
+        dense = {"impl": "flash_attn 2.8.3 flash_attn_with_kvcache (dense, contiguous cache)",
+                 "ms": float(np.median(dts))}
+        del kc, vc
+    except Exception as e:  # pragma: no cover - comparator unavailable
+        dense = {"error": str(e)[:160]}
     # algorithmic HBM bytes per step: per (sequence, group) the compressed keys
     # read by both scoring passes + K/V of the selected <= 96 blocks
     m1 = Lb.swattn_num_pooled(L, cfg.l_C1, cfg.s_C1)
@@ -87,7 +115,10 @@ def main():
                        "l2": "flushed between steps (256 MB write)"},
             "roofline": {"bound": "hbm", "achieved": bytes_step / (ms / 1e3) / 1e9, "peak": hbm,
                          "unit": "GB/s", "frac": bytes_step / (ms / 1e3) / 1e9 / hbm,
-                         "algorithmic_bytes_per_step": bytes_step}}
+                         "algorithmic_bytes_per_step": bytes_step},
+            "dense_decode_comparator": dense}
+    if "ms" in dense:
+        line["speedup_vs_dense_decode"] = dense["ms"] / ms
     print(json.dumps(line), flush=True)
 
 
