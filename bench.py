@@ -163,13 +163,20 @@ def run_ours(args):
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or args.cp_sharded:
+        if args.cp_sharded and ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    args.cp = args.cp or args.cp_sharded
     from paper_2509_24663_b200 import _lib
     from paper_2509_24663_b200.core import AttentionConfig, make_qkv
     from paper_2509_24663_b200.counts import (compress_bytes, dense_total_counts,
                                               selection_total_counts, sparse_total_counts)
-    from paper_2509_24663_b200.parallel import context_parallel_attend
+    from paper_2509_24663_b200.parallel import (context_parallel_attend,
+                                                context_parallel_attend_sharded, shard_rows)
     from paper_2509_24663_b200.switch import attend_host_chunked
 
     cfg = AttentionConfig()
@@ -184,8 +191,14 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     taken = _lib.ctypes.c_int32(0)
+    a_sh, b_sh = shard_rows(n, ws)[rank]
+    if args.cp_sharded:
+        Q_sh, K_sh, V_sh = (x[a_sh:b_sh].contiguous() for x in (Q, K, V))
 
     def step():
+        if args.cp_sharded:
+            context_parallel_attend_sharded(Q_sh, K_sh, V_sh, cfg, n)
+            return
         if args.cp:
             context_parallel_attend(Q, K, V, cfg, ws, rank, O=O_, lse=lse)
             return
@@ -229,7 +242,17 @@ def run_ours(args):
         Oh[r0:r1].copy_(O_[r0:r1], non_blocking=True)
         lh[r0:r1].copy_(lse[r0:r1], non_blocking=True)
 
+    def e2e_step_cp_sharded():
+        # sharded CP: each rank copies in only its rows of Q/K/V and returns
+        # its rows of O/lse (the all-gathers run on the device)
+        qd, kd, vd = (x[a_sh:b_sh].to("cuda", non_blocking=True) for x in (Qh, Kh, Vh))
+        o_sh, l_sh, _ = context_parallel_attend_sharded(qd, kd, vd, cfg, n)
+        Oh[a_sh:b_sh].copy_(o_sh, non_blocking=True)
+        lh[a_sh:b_sh].copy_(l_sh, non_blocking=True)
+
     def e2e_step():
+        if args.cp_sharded:
+            return e2e_step_cp_sharded()
         if args.cp:
             return e2e_step_cp()
         # the host-buffer entry point: K/V then Q chunks stream H2D on a copy
@@ -286,7 +309,10 @@ def run_ours(args):
             "config": {"workload": f"attend (sparse branch) prefill, n={n} tokens, batch 1 per GPU",
                        "n": n, "batch_per_gpu": 1, "h_q": 32, "h_kv": 2, "d_h": 128, "B": 64,
                        "budget_blocks": "1+32+63", "selection_mode": "approx",
-                       "parallelism": (f"context parallel: one sequence, cost-balanced query rows over "
+                       "parallelism": (f"context parallel, sequence-sharded inputs over {ws} rank(s): "
+                                       f"NCCL all-gather of the K halo, compressed keys and K/V"
+                                       if args.cp_sharded else
+                                       f"context parallel: one sequence, cost-balanced query rows over "
                                        f"{ws} rank(s), K/V replicated, no data-path collective"
                                        if args.cp else
                                        f"batch x kv-group sharding, {ws} rank(s), no collective"),
@@ -331,7 +357,7 @@ def run_ours(args):
         if not args.no_cpu and ws == 1:
             line["cpu_baseline"] = cpu_baseline_sample(n, rows_n=args.cpu_rows)
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 
@@ -500,6 +526,9 @@ def main():
     ap.add_argument("--cp", action="store_true",
                     help="context parallelism: all ranks share ONE n-token sequence, each "
                          "computes its cost-balanced query rows (strong scaling)")
+    ap.add_argument("--cp-sharded", action="store_true",
+                    help="context parallelism with sequence-sharded Q/K/V: per-shard K1, NCCL "
+                         "all-gather of compressed keys and K/V (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
