@@ -406,7 +406,9 @@ constexpr int kKvBuf = 4;    // queries in flight (cp.async prefetch depth): the
 struct __align__(128) DkvSmem {
   uint8_t q[kKvBuf][kG * kD * 2];   // 4 KB each, [head][d] swizzled (swz256)
   uint8_t go[kKvBuf][kG * kD * 2];
-  float lse[kKvBuf][kG], delta[kKvBuf][kG];
+  __align__(16) float lse[kKvBuf][kG];  // natural log, as stored by the forward
+  __align__(16) float delta[kKvBuf][kG];
+  int32_t tok[kSeg];                    // the segment's queries, ascending
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
@@ -435,8 +437,13 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
     for (int e = 0; e < 4; ++e) dk[j][e] = dv[j][e] = 0.f;
 
   const int64_t npairs = sg.end - sg.begin;
-  auto stage = [&](int64_t pi, int buf) {  // all 128 threads: Q_i, dO_i rows of group g
-    const int64_t i = (int64_t)(p.keys[sg.begin + pi] & 0xffffffffull);
+  // the segment's query ids once into shared memory (no dependent global
+  // load on the per-query path)
+  for (int t = threadIdx.x; t < npairs; t += blockDim.x)
+    sm.tok[t] = (int32_t)(p.keys[sg.begin + t] & 0xffffffffull);
+  __syncthreads();
+  auto stage = [&](int64_t pi, int buf) {  // all 128 threads: Q_i, dO_i, lse_i, delta_i of group g
+    const int64_t i = sm.tok[pi];
     const __nv_bfloat16 *qs = p.Q + (i * p.h_q + g * kG) * kD;
     const __nv_bfloat16 *gs = p.dO + (i * p.h_q + g * kG) * kD;
     for (int c = threadIdx.x; c < kG * 16; c += blockDim.x) {  // 16-byte chunks
@@ -444,9 +451,11 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
       cp_async16(tc::smem_u32(sm.q[buf]) + swz256(r, ch), qs + r * kD + ch * 8);
       cp_async16(tc::smem_u32(sm.go[buf]) + swz256(r, ch), gs + r * kD + ch * 8);
     }
-    if (threadIdx.x < kG) {
-      sm.lse[buf][threadIdx.x] = p.lse[i * p.h_q + g * kG + threadIdx.x] * kLog2e;
-      sm.delta[buf][threadIdx.x] = p.delta[i * p.h_q + g * kG + threadIdx.x];
+    if (threadIdx.x < 8) {  // 16 lse + 16 delta floats: 8 x 16 bytes
+      const int part = threadIdx.x & 3;
+      const float *src = (threadIdx.x < 4 ? p.lse : p.delta) + i * p.h_q + g * kG + part * 4;
+      float *dst = (threadIdx.x < 4 ? sm.lse[buf] : sm.delta[buf]) + part * 4;
+      cp_async16(tc::smem_u32(dst), src);
     }
     asm volatile("cp.async.commit_group;");
   };
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
     else asm volatile("cp.async.commit_group;");
     asm volatile("cp.async.wait_group %0;" ::"n"(kKvBuf - 1));  // query pi has landed
     __syncthreads();
-    const int64_t i = (int64_t)(p.keys[sg.begin + pi] & 0xffffffffull);
+    const int64_t i = sm.tok[pi];
     const uint32_t qb = tc::smem_u32(sm.q[buf]), gb_ = tc::smem_u32(sm.go[buf]);
     // S^T (16 keys x 16 heads) = K_w Q_i^T, dP^T = V_w dO_i^T
     float st[2][4], dpt[2][4];
@@ -494,7 +503,7 @@ __global__ void __launch_bounds__(kKvWarps * 32) bwd_dkdv_kernel(const __grid_co
         const int h = j * 8 + 2 * (lane & 3) + (e & 1);
         const int64_t key = key_w + (lane >> 2) + (e >= 2 ? 8 : 0);
         const bool vis = (p.mode == 2 || key <= i) && key < p.n;
-        const float pr = vis ? fast_exp2(fmaf(st[j][e], p.scale_log2, -sm.lse[buf][h])) : 0.f;
+        const float pr = vis ? fast_exp2(fmaf(st[j][e], p.scale_log2, -sm.lse[buf][h] * kLog2e)) : 0.f;
         pt[j][e] = pr;
         dst[j][e] = pr * (dpt[j][e] - sm.delta[buf][h]);
       }
