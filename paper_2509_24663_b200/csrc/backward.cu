@@ -38,7 +38,10 @@ constexpr int kBlk = 64;
 constexpr int kStageKeys = 16;
 constexpr int kStagesPerBlock = kBlk / kStageKeys;
 constexpr uint32_t kTileBytes = kStageKeys * kD * 2;  // 4 KB
-constexpr int kQWarps = 8;                             // B1 warps per CTA
+#ifndef SWATTN_BWD_QWARPS
+#define SWATTN_BWD_QWARPS 8
+#endif
+constexpr int kQWarps = SWATTN_BWD_QWARPS;             // B1 warps per CTA
 constexpr int kQStages = 2;
 constexpr int kSeg = 1024;                             // B3 queries per segment
 constexpr float kLog2e = 1.4426950408889634f;
