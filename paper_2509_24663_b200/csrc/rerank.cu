@@ -378,7 +378,7 @@ int32_t run_rerank(const RerankArgs &a, int num_sms, cudaStream_t stream) {
     rerank_p1_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);
     SWATTN_LAUNCH_CHECK("rerank_p1_kernel");
   }
-  rerank_kernel<<<num_sms, kThreads, smem, stream>>>(a);
+  rerank_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);  // 2 CTAs per SM (launch bounds)
   SWATTN_LAUNCH_CHECK("rerank_kernel");
   return SWATTN_OK;
 }
