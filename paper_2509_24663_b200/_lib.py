@@ -140,7 +140,22 @@ def check(rc: int, what: str) -> None:
     raise SwattnError(f"{what}: {msg}")
 
 
+_CFG_CACHE: dict = {}
+
+
 def c_config(cfg) -> CConfig:
+    """The C struct of an AttentionConfig (cached per config: the C side
+    only reads it)."""
+    try:
+        hit = _CFG_CACHE.get(cfg)
+    except TypeError:  # unhashable (a mutable stand-in): build it every time
+        return _build_c_config(cfg)
+    if hit is None:
+        hit = _CFG_CACHE[cfg] = _build_c_config(cfg)
+    return hit
+
+
+def _build_c_config(cfg) -> CConfig:
     c = CConfig()
     for name, _ in CConfig._fields_:
         if name == "scale_compressed_logits":

@@ -67,12 +67,16 @@ def attend(Q, K, V, cfg: AttentionConfig, policy: SwitchPolicy | None = None,
     lse = torch.empty((n, h_q), dtype=torch.float32, device=Qd.device)
     L = _lib.lib()
     c = _lib.c_config(cfg)
-    ws = Workspace.get(L.swattn_workspace_bytes(c, n), Qd.device)
     taken = _lib.ctypes.c_int32(0)
+    if mode == MODE_DENSE:   # K5 needs no workspace
+        ws_ptr, ws_bytes = None, 0
+    else:
+        ws = Workspace.get(L.swattn_workspace_bytes(c, n), Qd.device)
+        ws_ptr, ws_bytes = ws.data_ptr(), ws.numel()
     _lib.check(L.swattn_attend(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), n, int(threshold),
                                _lib.FORCED_MODE[mode], _lib.SELECT_MODE[selection_mode],
                                O.data_ptr(), lse.data_ptr(), _lib.ctypes.byref(taken),
-                               ws.data_ptr(), ws.numel(), _lib.stream_handle(Qd.device)),
+                               ws_ptr, ws_bytes, _lib.stream_handle(Qd.device)),
                "swattn_attend")
     assert taken.value == (1 if mode == MODE_DENSE else 2)
     return _finish(O, lse, host), mode
