@@ -190,6 +190,7 @@ __device__ __forceinline__ void mma16816_dec(float (&c)[4], const uint32_t (&a)[
 
 __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const float2 *part,
                                                            int splits, float *s_cmp, int64_t ld) {
+  __shared__ __align__(128) uint8_t ktile[kTileCols * 256];  // 32 KB of C1 rows
   __shared__ float2 stat[kG];  // (m, 1/l), log2 domain
   __shared__ float sc[kTileCols + 4];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
@@ -225,26 +226,44 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
     qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
     qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
   }
-  // B fragments: column (n) = lane / 4 of each 8-column n-tile, d = 16 ks + 2 (lane % 4)
-  const int64_t col0 = (int64_t)t * kTileBlocks * kPoolS + warp * 32;
+  // the tile's 128 C1 rows -> shared memory by cp.async (256-byte rows, 16-byte
+  // chunk c of row rr at c ^ (rr & 7): conflict-free ldmatrix), zeros past vis1
+  const int64_t tile0 = (int64_t)t * kTileBlocks * kPoolS;
   const __nv_bfloat16 *kbase = a.kc1 + ((int64_t)seq * a.max_m1 * a.h_kv + g) * kD;
+  const uint32_t kt = tc::smem_u32(ktile);
+  for (int c = threadIdx.x; c < kTileCols * 16; c += blockDim.x) {
+    const int rr = c >> 4, ch = c & 15;
+    const uint32_t dst = kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4);
+    const int64_t col = tile0 + rr;
+    if (col < vis1)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(kbase + col * a.h_kv * kD + ch * 8));
+    else
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0u));
+  }
+  asm volatile("cp.async.commit_group;");
+  asm volatile("cp.async.wait_group 0;");
+  const int64_t col0 = tile0 + warp * 32;
   float acc[4][4];
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-    const int64_t col = col0 + nt * 8 + r;
-    const bool ok = col < vis1;  // invisible / missing columns are masked below
-    const uint32_t *kr = reinterpret_cast<const uint32_t *>(kbase + (ok ? col : 0) * a.h_kv * kD);
-    uint32_t kb[8][2];
+  for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+  __syncthreads();  // tile and stat
+  const int lm = lane >> 3, lr = lane & 7;
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      kb[ks][0] = ok ? __ldg(kr + ks * 8 + dw) : 0u;
-      kb[ks][1] = ok ? __ldg(kr + ks * 8 + 4 + dw) : 0u;
+  for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      // rows (columns) 32 warp + 16 hf + 8 (lm >> 1) + lr; matrices (n-tile lo, k lo),
+      // (n-tile lo, k hi), (n-tile hi, k lo), (n-tile hi, k hi)
+      const int rr = warp * 32 + hf * 16 + (lm >> 1) * 8 + lr, ch = ks * 2 + (lm & 1);
+      uint32_t b00, b01, b10, b11;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(b00), "=r"(b01), "=r"(b10), "=r"(b11)
+                   : "r"(kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4)));
+      mma16816_dec(acc[2 * hf], qa[ks], b00, b01);
+      mma16816_dec(acc[2 * hf + 1], qa[ks], b10, b11);
     }
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) mma16816_dec(acc[nt], qa[ks], kb[ks][0], kb[ks][1]);
   }
-  __syncthreads();  // stat
   const float2 st0 = stat[r], st1 = stat[r + 8];
 #pragma unroll
   for (int nt = 0; nt < 4; ++nt) {
