@@ -111,6 +111,9 @@ __device__ __forceinline__ void fa_item(const FaParams &p, int64_t w, int &tile,
   tile = p.tile_end - 1 - (int)(w % p.n_tiles);
 }
 
+// kPersist = false: one item per CTA (the grid covers the items); the item
+// loops below then run once and the running counters fold to constants.
+template <bool kPersist>
 __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_constant__ FaParams p) {
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on smem_raw so accesses stay in the shared space
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     }
     uint32_t gi0 = 0;
     int it = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
       int tile, g;
       fa_item(p, w, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     const uint32_t q_addr = tc::smem_u32(s.q);
     uint32_t gi0 = 0;
     int it = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
       int tile, g;
       fa_item(p, w, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     uint32_t gi0 = 0;
     int it = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
       int tile, g;
       fa_item(p, w, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
@@ -435,7 +438,8 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   const size_t smem = sizeof(FaSmem) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fa_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fa_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fa_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   // persistent: two CTAs per SM walk the (tile, group) items
@@ -453,9 +457,12 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   // 119 ms one-per-item vs 145 ms persistent).
   const int64_t items = (int64_t)p.n_tiles * cfg->h_kv;
   constexpr int64_t kPersistItems = 8192;
-  const int64_t grid = items > kPersistItems ? items
-                                             : (items < 2 * (int64_t)sms ? items : 2 * (int64_t)sms);
-  fa_tile_kernel<<<(unsigned)grid, kThreads, smem, stream>>>(p);
+  if (items > kPersistItems) {
+    fa_tile_kernel<false><<<(unsigned)items, kThreads, smem, stream>>>(p);
+  } else {
+    const int64_t grid = items < 2 * (int64_t)sms ? items : 2 * (int64_t)sms;
+    fa_tile_kernel<true><<<(unsigned)grid, kThreads, smem, stream>>>(p);
+  }
   SWATTN_LAUNCH_CHECK("fa_tile_kernel");
   return SWATTN_OK;
 }
