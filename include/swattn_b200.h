@@ -13,10 +13,14 @@
  *      Q [n, h_q, d_h], K/V [n, h_kv, d_h], bf16 (core.py:6-7)
  *    query head h reads KV head h / (h_q/h_kv) (dense.py:11-13);
  *  - outputs and the workspace are allocated by the caller; the library
- *    allocates nothing and keeps no global state except the thread-local
- *    error message;
+ *    allocates no device memory and keeps no global state except the
+ *    thread-local error message and, per host thread and device, one side
+ *    stream with two events (swattn_attend / swattn_attend_rows run K4 part A
+ *    on it beside the selection kernels, joined back into `stream` before
+ *    the call's last kernel);
  *  - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
- *    default stream); no implicit device synchronisation;
+ *    default stream); no implicit device synchronisation (exception: the
+ *    backward entry points read the data-dependent pair count back once);
  *  - return value: SWATTN_OK or an error code; swattn_last_error() holds the
  *    message (same invariant-prefixed wording as the reference's ConfigError
  *    / ValueError / RuntimeError, core.py:118-175, dense.py:36-56).
