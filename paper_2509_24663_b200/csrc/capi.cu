@@ -7,6 +7,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace swattn {
@@ -412,11 +414,12 @@ struct SideStream {
 };
 
 static int32_t side_stream(SideStream *&out) {
-  thread_local SideStream ss[16];
+  thread_local std::vector<SideStream> ss;  // one per device, created on first use
   int dev = 0;
   int32_t rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   if (rc) return rc;
-  SideStream &x = ss[dev & 15];
+  if ((size_t)dev >= ss.size()) ss.resize((size_t)dev + 1);
+  SideStream &x = ss[(size_t)dev];
   if (x.device != dev) {
     if ((rc = cuda_check(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking), "side stream")) ||
         (rc = cuda_check(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming), "side event")) ||
