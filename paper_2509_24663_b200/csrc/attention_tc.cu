@@ -298,15 +298,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
           for (int c = 0; c < kBlk; ++c)
             if (c > lim) x[c] = -INFINITY;
         }
-        float mx0 = x[0], mx1 = x[1], mx2 = x[2], mx3 = x[3];
-#pragma unroll
-        for (int c = 4; c < kBlk; c += 4) {
-          mx0 = fmaxf(mx0, x[c]);
-          mx1 = fmaxf(mx1, x[c + 1]);
-          mx2 = fmaxf(mx2, x[c + 2]);
-          mx3 = fmaxf(mx3, x[c + 3]);
-        }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.scale_log2;
+        const float mx = max64(x) * p.scale_log2;
         // Lazy rescale.  tcgen05.ld / st are warp-collective (.sync.aligned), so
         // the O read-modify-write runs for the whole warp whenever any of its
         // rows needs it; rows that do not scale by 1.

@@ -38,6 +38,24 @@ struct Dims {
 // ---------------------------------------------------------------- small device helpers
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
 
+// three-input max (one FMNMX3 on sm_100; NaN-ignoring like fmaxf)
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// max of 64 values in 32 FMNMX3 (two independent chains)
+__device__ __forceinline__ float max64(const float (&x)[64]) {
+  float m0 = x[0], m1 = x[1];
+#pragma unroll
+  for (int c = 2; c < 62; c += 4) {
+    m0 = fmax3f(m0, x[c], x[c + 1]);
+    m1 = fmax3f(m1, x[c + 2], x[c + 3]);
+  }
+  return fmax3f(m0, m1, fmaxf(x[62], x[63]));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -222,15 +222,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
         for (int e = 0; e < 64; ++e)
           if (e >= lim) x[e] = -INFINITY;
       }
-      float cm0 = x[0], cm1 = x[1], cm2 = x[2], cm3 = x[3];
-#pragma unroll
-      for (int e = 4; e < 64; e += 4) {
-        cm0 = fmaxf(cm0, x[e]);
-        cm1 = fmaxf(cm1, x[e + 1]);
-        cm2 = fmaxf(cm2, x[e + 2]);
-        cm3 = fmaxf(cm3, x[e + 3]);
-      }
-      const float cm = fmaxf(fmaxf(cm0, cm1), fmaxf(cm2, cm3)) * p.scale_log2;
+      const float cm = max64(x) * p.scale_log2;
       if (cm > m) {
         l *= fast_exp2(m - cm);
         m = cm;
