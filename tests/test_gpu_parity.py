@@ -249,7 +249,10 @@ def test_full_size_properties_and_sampled_rows(n, seed):
     t = np.where(valid, top, np.iinfo(np.int32).max)
     assert np.all(np.diff(t, axis=2)[valid[:, :, 1:]] > 0)
     assert np.all((top >= 1)[valid]) and np.all((top < lo[None, :, None])[valid])
-    rows = _random_rows(n, 24, seed)
+    # 96 random rows plus the first rows with a competitive top-k (query block
+    # 96: candidates just above k) and the last query block
+    rows = np.unique(np.concatenate([_random_rows(n, 96, seed), np.arange(96 * 64, 96 * 64 + 4),
+                                     np.arange(n - 4, n)]))
     want_top, _, _ = O.select(Q, K, prof, "approx", rows=rows)
     assert np.array_equal(top[:, rows, :], want_top)
     full = np.full((2, n, 63), -1, dtype=np.int64)
