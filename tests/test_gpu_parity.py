@@ -446,3 +446,28 @@ def test_large_logits_dense_and_part_a(scale):
     topk = sel.topk.cpu().numpy().astype(np.int64)
     want_o, want_l = O.sparse_attention(Qs, K, V, topk, prof, rows=rows)
     _tol(res.output[r], want_o, res.lse[r], want_l)
+
+
+@pytest.mark.gpu
+def test_attend_cuda_graph_capture():
+    """The sparse attend (K1..K4, part A forked onto the library's side stream
+    and joined back) can be captured in a CUDA graph and replayed -- the
+    serving path -- with results bit-identical to the eager call."""
+    from paper_2509_24663_b200.core import make_qkv
+    cfg = AttentionConfig()
+    n = 16384
+    Q, K, V = make_qkv(n, 32, 2, 128, seed=4)
+    eager, _ = attend(Q, K, V, cfg, SwitchPolicy(forced_mode="sparse"))
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        attend(Q, K, V, cfg, SwitchPolicy(forced_mode="sparse"))   # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        res, _ = attend(Q, K, V, cfg, SwitchPolicy(forced_mode="sparse"))
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(res.output, eager.output) and torch.equal(res.lse, eager.lse)
