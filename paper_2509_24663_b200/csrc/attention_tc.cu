@@ -104,6 +104,13 @@ __device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t
 // the previous item's last S MMA completed (q_empty); the first PV of an
 // item waits until the softmax warps have read the previous O out of TMEM
 // (o_empty).  TMEM is allocated once per CTA.
+// Persistent CTAs take the items in zig-zag rounds (CTA c gets c, 2G-1-c,
+// 2G+c, ...), so every CTA's heavy-first share sums to about the same work.
+__device__ __forceinline__ int64_t fa_slot_item(int64_t w, int64_t n_items) {
+  const int64_t G = gridDim.x, r = w / G, c = w % G;
+  return ((r & 1) && (r + 1) * G <= n_items) ? r * G + (G - 1 - c) : w;
+}
+
 __device__ __forceinline__ void fa_item(const FaParams &p, int64_t w, int &tile, int &g) {
   // group-major (one group's K/V, 67 MB at 128K, stays L2-resident while its
   // tiles run), heavy (late) tiles first within a group
@@ -161,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     int it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
       int tile, g;
-      fa_item(p, w, tile, g);
+      fa_item(p, kPersist ? fa_slot_item(w, n_items) : w, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
       const BlockList L = make_list(p, (int)(t0 / kBlk), nb_total);
       const int nblk = L.size();
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     int it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
       int tile, g;
-      fa_item(p, w, tile, g);
+      fa_item(p, kPersist ? fa_slot_item(w, n_items) : w, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
       const BlockList L = make_list(p, (int)(t0 / kBlk), nb_total);
       const int nblk = L.size();
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     int it = 0;
     for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
       int tile, g;
-      fa_item(p, w, tile, g);
+      fa_item(p, kPersist ? fa_slot_item(w, n_items) : w, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
       const BlockList L = make_list(p, (int)(t0 / kBlk), nb_total);
       const int nblk = L.size();
@@ -448,7 +455,10 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   // item lets the block scheduler balance the long causal rows (128K dense:
   // 119 ms one-per-item vs 145 ms persistent).
   const int64_t items = (int64_t)p.n_tiles * cfg->h_kv;
-  constexpr int64_t kPersistItems = 8192;
+#ifndef SWATTN_FA_PERSIST_ITEMS
+#define SWATTN_FA_PERSIST_ITEMS 8192
+#endif
+  constexpr int64_t kPersistItems = SWATTN_FA_PERSIST_ITEMS;
   if (items > kPersistItems) {
     fa_tile_kernel<false><<<(unsigned)items, kThreads, smem, stream>>>(p);
   } else {
