@@ -508,21 +508,30 @@ __global__ void __launch_bounds__(512) decode_combine_kernel(DecodeArgs a, const
   const int n_init = min(a.N_init, b + 1);
   const int lo2 = max(max(0, b - a.N_local + 1), n_init);
   const int nvis = n_init + topk_cnt[row] + (b + 1 - lo2);
-  const int used = (int)cdiv(nvis, kAttnBlocks);
-  float M = -INFINITY;
-  for (int sp = 0; sp < used; ++sp) M = fmaxf(M, part_ml[((int64_t)row * splits + sp) * kG + h].x);
-  float Ls = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int used = (int)cdiv(nvis, kAttnBlocks);  // <= 24 splits (96 blocks / 4)
+  // lane s holds split s's (max, sum): one load, then warp reductions
+  float2 ml = make_float2(-INFINITY, 0.f);
+  if (lane < used) ml = part_ml[((int64_t)row * splits + lane) * kG + h];
+  float M = ml.x;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const float wl = ml.x == -INFINITY ? 0.f : fast_exp2(ml.x - M);
+  float Ls = ml.y * wl;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, off);
+  // the splits' partial O rows are independent loads (4 in flight)
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
   for (int sp = 0; sp < used; ++sp) {
+    const float w = __shfl_sync(0xffffffffu, wl, sp);
     const int64_t pi = ((int64_t)row * splits + sp) * kG + h;
-    const float2 ml = part_ml[pi];
-    if (ml.x == -INFINITY) continue;
-    const float w = fast_exp2(ml.x - M);
-    Ls += ml.y * w;
     const float4 po = *reinterpret_cast<const float4 *>(&part_o[pi * kD + 4 * lane]);
-    acc[0] += po.x * w;
-    acc[1] += po.y * w;
-    acc[2] += po.z * w;
-    acc[3] += po.w * w;
+    if (w != 0.f) {
+      acc[0] += po.x * w;
+      acc[1] += po.y * w;
+      acc[2] += po.z * w;
+      acc[3] += po.w * w;
+    }
   }
   const float inv = 1.f / Ls;
   __nv_bfloat16 *dst = o + ((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane;
