@@ -1,8 +1,9 @@
 // K5 / K4-part-A -- block-list flash attention on tcgen05 (sm_100a).
 //
-// One CTA = one GQA-packed query tile of 128 rows = 8 tokens x 16 heads of
-// one KV group (row r <-> token t0 + r/16, head 16g + r%16), so every row of
-// the tile reads the same K/V blocks.  The tile walks a list of 64-key
+// One work item = one GQA-packed query tile of 128 rows = 8 tokens x 16 heads
+// of one KV group (row r <-> token t0 + r/16, head 16g + r%16), so every row
+// of the tile reads the same K/V blocks.  Up to 8192 items the CTAs are
+// persistent (two per SM walk the items); above that one CTA per item.  The tile walks a list of 64-key
 // blocks:
 //   dense (tiled_gqa_forward, dense.py:112-170): blocks 0..b, causal;
 //   sparse part A (sparse.py:43-98, the init + local blocks every token of a
@@ -16,10 +17,11 @@
 //               double-buffered TMEM S tile (128 x 64 fp32), then
 //               O += P_{j-1} V_{j-1} with P read straight from TMEM (kind::f16
 //               A-from-TMEM), O accumulated in TMEM (128 x 128 fp32);
-//   warps 2..5  softmax: thread = row; online max with lazy rescaling (O is
-//               rescaled in TMEM only when the row max grows by > 2^8),
-//               P = exp2(s*scale*log2e - m) packed to bf16 into the S buffer;
-//               epilogue O / l -> bf16, lse.
+//   warps 2..5  softmax: thread = row; online max (FMNMX3) with lazy
+//               rescaling (O is rescaled in TMEM only when the row max grows
+//               by > 2^8, warp-collectively), P = exp2(s*scale*log2e - m)
+//               (one FFMA + ex2) packed to bf16 into the S buffer; epilogue
+//               O / l -> bf16, lse.
 // Roofline: tensor-bound; algorithmic FLOP = 4 * visible_pairs * d_h * h_q
 // (dense.py:167-169 counts x 2).
 #include <string.h>
