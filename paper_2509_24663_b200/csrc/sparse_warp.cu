@@ -67,7 +67,7 @@ constexpr int kBlk = 64;
 constexpr int kStagesPerBlock = kBlk / kStageKeys;       // 4
 constexpr uint32_t kTileBytes = kStageKeys * kD * 2;     // 4 KB (K or V of one stage)
 constexpr uint32_t kQBytes = kG * kD * 2;                // 4 KB
-constexpr float kOverflowExcess = 64.f;
+constexpr float kOverflowSum = 1.8446744073709552e19f;  // 2^64
 
 struct PwParams {
   CUtensorMap q_map;  // Q as (d lo/hi 64, head, half, token): box {64, 16, 2, 1}
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     }
 #endif
     const float mA0 = p.m_a[ridx + h0], mA1 = p.m_a[ridx + h0 + 8];
-    float lp0 = 0.f, lp1 = 0.f, excess = -INFINITY;
+    float lp0 = 0.f, lp1 = 0.f;
     float o[16][4];
 #pragma unroll
     for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
@@ -298,7 +298,6 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
         x[j][1] = fmaf(sc[j][1], p.scale_log2, -mA0);
         x[j][2] = fmaf(sc[j][2], p.scale_log2, -mA1);
         x[j][3] = fmaf(sc[j][3], p.scale_log2, -mA1);
-        excess = fmaxf(excess, fmaxf(fmaxf(x[j][0], x[j][1]), fmaxf(x[j][2], x[j][3])));
 #pragma unroll
         for (int e = 0; e < 4; ++e) x[j][e] = fast_exp2(x[j][e]);
         lp0 += x[j][0] + x[j][1];
@@ -330,8 +329,11 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     lp0 += __shfl_xor_sync(0xffffffffu, lp0, 2);
     lp1 += __shfl_xor_sync(0xffffffffu, lp1, 1);
     lp1 += __shfl_xor_sync(0xffffffffu, lp1, 2);
-    for (int off = 16; off; off >>= 1) excess = fmaxf(excess, __shfl_xor_sync(0xffffffffu, excess, off));
-    if (excess > kOverflowExcess && lane == 0) {
+    // overflow guard without a per-element max: any logit more than 64
+    // (log2) above m_A makes its p > 2^64, so the row sum exceeds it too
+    // (the test is conservative: huge sums of smaller p's are caught as well)
+    const bool big = !(lp0 <= kOverflowSum) || !(lp1 <= kOverflowSum);  // also inf / NaN
+    if (__any_sync(0xffffffffu, big) && lane == 0) {
       const int slot = atomicAdd(p.slow_count, 1);
       p.slow_list[slot] = (int32_t)row;
     }

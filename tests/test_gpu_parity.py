@@ -471,3 +471,27 @@ def test_attend_cuda_graph_capture():
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(res.output, eager.output) and torch.equal(res.lse, eager.lse)
+
+
+@pytest.mark.gpu
+def test_part_b_overflow_slow_path():
+    """A top-k key whose logit exceeds the part-A offset m_A by far more than
+    2^64 (log2) overflows part B's fixed-offset softmax; the token must go
+    through the exact CUDA-core path and still match the float64 oracle."""
+    n = 8192
+    cfg = AttentionConfig()
+    prof = O.Profile()
+    Q, K, V = O.draw_qkv(n, 32, 2, 128, 13)
+    i, j = 8000, 40                                   # query block 125, candidate block 40
+    K = K.copy()
+    K[j * 64 + 5, 0] = (Q[i, 0].astype(np.float32) * 8.0).astype(K.dtype)   # huge logit, head 0
+    Qd, Kd, Vd = _dev(Q), _dev(K), _dev(V)
+    res, mode = attend(Qd, Kd, Vd, cfg, SwitchPolicy(forced_mode="sparse"))
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    torch.cuda.synchronize()
+    top = sel.topk.cpu().numpy().astype(np.int64)
+    assert j in top[0, i]
+    rows = np.array([i, i - 1, i + 1])
+    want_o, want_l = O.sparse_attention(Q, K, V, top, prof, rows=rows)
+    r = torch.as_tensor(rows, device="cuda")
+    _tol(res.output[r], want_o, res.lse[r], want_l)
