@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
   prod.it = (int64_t)blockIdx.x * kWarps + warp;
   prod.load(p, lane);
   if (!prod.valid(p)) return;
-  int64_t issued = 0;  // stages issued (ring position)
+  uint32_t issued = 0;  // stages issued (ring position; only its low bits matter)
   auto issue = [&]() {
     const int blk = prod.block();
     if (lane == 0) {
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
   const int h0 = lane >> 2;  // rows (heads) h0 and h0 + 8 of every fragment
   // ldmatrix lane roles: matrix m = lane / 8, row-in-matrix = lane % 8
   const int lm = lane >> 3, lr = lane & 7;
-  int64_t consumed = 0;
+  uint32_t consumed = 0;
   int64_t qphase = 0;
   Stream cons;
   cons.it = (int64_t)blockIdx.x * kWarps + warp;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     const int nst = cons.cnt * kStagesPerBlock;
     for (int s = 0; s < nst; ++s, ++consumed) {
       const int st = (int)(consumed % kStages);
-      tc::mbar_wait(&full[st], (uint32_t)((consumed / kStages) & 1));
+      tc::mbar_wait(&full[st], (consumed / kStages) & 1u);
       const uint32_t kst = kbase + st * kTileBytes, vst = vbase + st * kTileBytes;
 #pragma unroll
       for (int sub = 0; sub < kStageKeys / 16; ++sub) {
