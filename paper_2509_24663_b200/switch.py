@@ -155,9 +155,9 @@ def chunk_bounds(n: int, B: int, rows: int | None = None) -> list[tuple[int, int
 def attend_host_chunked(Q, K, V, cfg: AttentionConfig, selection_mode: str = "approx",
                         out=None, chunk_rows: int | None = None, device=None):
     """Sparse branch of attend for HOST inputs with the host<->device copies
-    overlapped with compute: K and V go over first (K1 needs all of K), then
-    Q streams in row chunks on a copy stream while the compute stream runs
-    select + sparse attention for the chunks already resident
+    overlapped with compute: Q, K and V stream in row chunks on a copy stream
+    while the compute stream pools the compressed keys of the rows already
+    resident and runs select + sparse attention for those chunks
     (swattn_attend_rows), and a second copy stream returns O / lse of each
     finished chunk.  Returns pinned host (O bf16 [n, h_q, d_h], lse fp32
     [n, h_q]); `out` may pass them in.  Rows are computed exactly as by the
@@ -182,18 +182,33 @@ def attend_host_chunked(Q, K, V, cfg: AttentionConfig, selection_mode: str = "ap
     bounds = chunk_bounds(n, cfg.B, chunk_rows)
     s_in.wait_stream(comp)   # device buffers may still be read by the previous call
     s_out.wait_stream(comp)
+    # Q, K and V all stream in row chunks: chunk c needs K / V rows < r1 only
+    # (causal), and the compressed keys of its rows are pooled from K[:r1] as
+    # it arrives (windows that end by r1; the window halo is re-pooled from
+    # 64 rows before the chunk, bit-identically), so compute starts after the
+    # first chunk instead of after all of K and V.
     with torch.cuda.stream(s_in):
-        Kd.copy_(Kh, non_blocking=True)
-        Vd.copy_(Vh, non_blocking=True)
         q_ready = []
         for r0, r1 in bounds:
+            Kd[r0:r1].copy_(Kh[r0:r1], non_blocking=True)
+            Vd[r0:r1].copy_(Vh[r0:r1], non_blocking=True)
             Qd[r0:r1].copy_(Qh[r0:r1], non_blocking=True)
             e = torch.cuda.Event()
             e.record(s_in)
             q_ready.append(e)
-    sel = _lib.SELECT_MODE[selection_mode]
+    sel = _lib.SELECT_MODE[selection_mode] | _lib.SELECT_PREPARED
+    p1, p2 = _lib.ctypes.c_void_p(), _lib.ctypes.c_void_p()
+    _lib.check(L.swattn_workspace_ckeys(c, n, ws.data_ptr(), _lib.ctypes.byref(p1),
+                                        _lib.ctypes.byref(p2)), "swattn_workspace_ckeys")
+    row_b = h_kv * d_h * 2
+    halo = max(cfg.l_C1 - cfg.s_C1, cfg.l_C2 - cfg.s_C2)
     for (r0, r1), e in zip(bounds, q_ready):
         comp.wait_event(e)
+        a = max(0, r0 - halo)   # a multiple of both pooling strides (chunks start on B)
+        _lib.check(L.swattn_compress_keys(c, Kd.data_ptr() + a * row_b, r1 - a,
+                                          p1.value + (a // cfg.s_C1) * row_b,
+                                          p2.value + (a // cfg.s_C2) * row_b, comp.cuda_stream),
+                   "swattn_compress_keys")
         _lib.check(L.swattn_attend_rows(c, Qd.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), n, r0, r1,
                                         sel, Od.data_ptr(), ld.data_ptr(), ws.data_ptr(),
                                         ws.numel(), comp.cuda_stream), "swattn_attend_rows")
