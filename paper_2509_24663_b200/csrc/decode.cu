@@ -203,16 +203,27 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
   if (t * kTileBlocks >= hi) return;
   const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kG) {
-    const int h = threadIdx.x;
-    float M = -INFINITY;
-    for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, part[((int64_t)row * splits + sp) * kG + h].x);
-    float S = 0.f;
-    for (int sp = 0; sp < splits; ++sp) {
+  if (warp == 0) {
+    // pass-1 partials of this row: only the slices pass 1 covered hold data
+    // (C2 columns for approx rows, C1 for fallback rows); lane pairs (h, half)
+    // merge half of the slices each, then one shuffle joins the halves
+    const int64_t vis2 = vis_count(i, a.l_C2, a.s_C2);
+    const int used = (int)min((int64_t)splits, cdiv(vis2 > 0 ? vis2 : vis1, (int64_t)kP1Cols));
+    const int h = lane & 15, half = lane >> 4;
+    float M = -INFINITY, S = 0.f;
+    for (int sp = half; sp < used; sp += 2) {
       const float2 pv = part[((int64_t)row * splits + sp) * kG + h];
-      if (pv.x != -INFINITY) S += pv.y * fast_exp2(pv.x - M);
+      if (pv.x == -INFINITY) continue;
+      const float Mn = fmaxf(M, pv.x);
+      S = (M == -INFINITY ? 0.f : S * fast_exp2(M - Mn)) + pv.y * fast_exp2(pv.x - Mn);
+      M = Mn;
     }
-    stat[h] = make_float2(M == -INFINITY ? 0.f : M, S > 0.f ? 1.f / S : 0.f);
+    const float oM = __shfl_xor_sync(0xffffffffu, M, 16), oS = __shfl_xor_sync(0xffffffffu, S, 16);
+    const float Mt = fmaxf(M, oM);
+    float St = 0.f;
+    if (Mt != -INFINITY)
+      St = (M == -INFINITY ? 0.f : S * fast_exp2(M - Mt)) + (oM == -INFINITY ? 0.f : oS * fast_exp2(oM - Mt));
+    if (half == 0) stat[h] = make_float2(Mt == -INFINITY ? 0.f : Mt, St > 0.f ? 1.f / St : 0.f);
   }
   // q as A fragments: a0 = (head r, d k), a1 = (r + 8, k), a2 = (r, k + 8), a3 = (r + 8, k + 8)
   const int r = lane >> 2, dw = lane & 3;
