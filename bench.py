@@ -6,13 +6,21 @@ GQA: h_q=32, h_kv=2, d_h=128, B=64, |I|=1+32+63) on B200.
 A step = one `attend` over one 128K-token sequence (K1 compress -> K2 block
 scoring -> K3 top-k (+ float64 boundary re-rank) -> K4 block-sparse
 attention), synthetic make_qkv inputs resident in HBM (Q alone is 1 GiB >
-L2, so no explicit flush is needed).  N>1: one process per GPU (torchrun),
-each rank serves its own sequence (batch x KV-group sharding, no
-collective; weak scaling); time = max over ranks of the device time.
+L2, so no explicit flush is needed).
+
+--gpus N > 1: bench.py re-executes itself under torch.distributed.run (one
+process per GPU, NCCL) unless it already runs under it.  Headline (weak
+scaling): each rank serves its own sequence -- batch sharding, no
+data-path collective; time = max over ranks of the device time.  The same
+line carries `strong_scaling`: ONE 128K sequence split over the N ranks by
+KV group (swattn_attend_rows_groups: rank r runs group r % h_kv) and
+cost-balanced query-row ranges (context parallelism over replicated K/V, no
+data-path collective).
 
 `--impl reference` times the CPU oracle port (oracle/swattn_oracle.py, a
-float64 numpy restatement of the reference's select_blocks + sparse_forward)
-on a bounded row sample of the same workload, on rank 0 only.
+float64 numpy restatement of the reference's select_blocks + sparse_forward;
+the reference is pure Python, nothing to compile) on whole query blocks of
+the same workload, on rank 0 only.
 """
 
 from __future__ import annotations
@@ -97,65 +105,154 @@ def _dist():
 
 # ----------------------------------------------------------------------------- reference arm
 
+class _PortSampler:
+    """The oracle port timed on WHOLE query blocks (64 contiguous rows, the
+    reference's B_q tile, selection.py:170-196) of the n-token workload, so the
+    per-tile amortisation of the reference is kept.  The sequence-wide
+    one-time work of one attend (pooling both key sets, selection.py:371-381;
+    the float64 casts of Q / K / V, selection.py:311, sparse.py:62-64) is timed
+    once and charged to every block by its 1/(n/64) share."""
+
+    def __init__(self, n, seed=0):
+        from oracle import swattn_oracle as O
+        self.O, self.cfg, self.n = O, O.PAPER, n
+        self.Q, self.K, self.V = O.draw_qkv(n, 32, 2, 128, seed=seed)
+        t0 = time.perf_counter()
+        self.ck1 = O.pool(self.K, self.cfg.l_C1, self.cfg.s_C1)
+        self.ck2 = O.pool(self.K, self.cfg.l_C2, self.cfg.s_C2)
+        self.Q64 = self.Q.astype(np.float64)
+        self.K64 = self.K.astype(np.float64)
+        self.V64 = self.V.astype(np.float64)
+        self.once_s = time.perf_counter() - t0
+        self.nb = -(-n // self.cfg.B)
+
+    def block(self, b):
+        """Seconds for query block b (select approx + sparse_forward) incl. its
+        share of the one-time work."""
+        O, cfg = self.O, self.cfg
+        rows = np.arange(b * cfg.B, min((b + 1) * cfg.B, self.n))
+        t0 = time.perf_counter()
+        S, nv = O.shared_scores(self.Q64, None, cfg, "approx", rows=rows, chunk=64,
+                                ck1=self.ck1, ck2=self.ck2)
+        scmp = O.block_scores(S, cfg.l, cfg.s)
+        top, _ = O.topk_blocks(scmp, nv, rows, self.n, cfg)
+        O.sparse_attention(self.Q64, self.K64, self.V64, _RowTopk(top, rows), cfg, rows=rows)
+        return time.perf_counter() - t0 + self.once_s * rows.size / self.n
+
+    def stratified(self, k, offset=0.5):
+        """k query blocks spread evenly over the sequence (cost grows with b)."""
+        return [min(self.nb - 1, int((s + offset) * self.nb / k)) for s in range(k)]
+
+
+class _RowTopk:
+    """topk[g, i] view over a row sample (no [h_kv, n, k] allocation)."""
+
+    def __init__(self, top, rows):
+        self.top, self.pos = top, {int(r): j for j, r in enumerate(rows)}
+
+    def __getitem__(self, gi):
+        g, i = gi
+        return self.top[g, self.pos[int(i)]]
+
+
+def _threads():
+    return int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    from oracle import swattn_oracle as O
-    cfg = O.PAPER
     n = args.n
-    Q, K, V = O.draw_qkv(n, 32, 2, 128, seed=0)
-    rng = np.random.default_rng(0)
-    R = args.cpu_rows
-    samples = []
-    for step in range(args.warmup + args.steps):
-        rows = np.sort(rng.choice(n, size=R, replace=False))
-        t0 = time.perf_counter()
-        top, _, _ = O.select(Q, K, cfg, "approx", rows=rows)
-        full = np.full((2, n, 63), -1, dtype=np.int64)
-        full[:, rows] = top
-        O.sparse_attention(Q, K, V, full, cfg, rows=rows)
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            samples.append(R / dt)
-    v = statistics.median(samples)
-    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    smp = _PortSampler(n, seed=0)
+    for b in smp.stratified(args.warmup, offset=0.21):   # warm-up blocks (untimed)
+        smp.block(b)
+    timed = [smp.block(b) for b in smp.stratified(args.steps)]
+    step_s = float(np.mean(timed))
+    v = 64 / step_s
     line = {
         "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * R / v,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_s,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (make_qkv Philox, bf16-rounded)", "impl": "reference",
-        "config": {"workload": f"attend sparse prefill n={n}, batch 1, paper profile",
-                   "n": n, "rows_per_step": R},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"{R} uniformly sampled query rows of the n={n} sequence "
-                                   "per step (select_blocks approx + sparse_forward rows), "
-                                   "numpy float64 oracle port of the reference"},
+        "data": "synthetic (make_qkv Philox normal(0,1), bf16-rounded)", "impl": "reference",
+        "config": {"workload": f"attend (sparse branch) prefill, n={n} tokens, batch 1, paper profile",
+                   "n": n, "step": "one query block (64 rows) of the n-token attend, blocks "
+                                   "stratified over the sequence, + its 64/n share of the "
+                                   "sequence-wide pooling / float64 casts"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": _threads(), "kind": "port",
+                         "sample": f"{args.steps} whole query blocks (64 rows each) of the n={n} "
+                                   f"sequence, stratified over positions; one-time work "
+                                   f"{smp.once_s:.2f} s amortised; numpy float64 oracle port of "
+                                   "select_blocks(approx) + sparse_forward"},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(n, rows_n=96, seed=0):
-    """The oracle port on a bounded row sample (rank 0, N=1)."""
-    from oracle import swattn_oracle as O
-    cfg = O.PAPER
-    Q, K, V = O.draw_qkv(n, 32, 2, 128, seed=seed)
-    rows = np.sort(np.random.default_rng(seed).choice(n, size=rows_n, replace=False))
-    t0 = time.perf_counter()
-    top, _, _ = O.select(Q, K, cfg, "approx", rows=rows)
-    full = np.full((2, n, 63), -1, dtype=np.int64)
-    full[:, rows] = top
-    O.sparse_attention(Q, K, V, full, cfg, rows=rows)
-    dt = time.perf_counter() - t0
-    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": rows_n / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{rows_n} uniformly sampled query rows of the n={n} workload "
-                      f"(select_blocks approx + sparse_forward), {dt:.1f} s, numpy float64 "
-                      "oracle port of the reference"}
+def cpu_baseline_sample(n, blocks=4, seed=0):
+    """The oracle port on a few whole query blocks (rank 0, N=1)."""
+    smp = _PortSampler(n, seed=seed)
+    bl = smp.stratified(blocks)
+    t = [smp.block(b) for b in bl]
+    v = 64 * len(t) / sum(t)
+    return {"value": v, "unit": "tokens/s", "cores": _threads(), "kind": "port",
+            "sample": f"{len(t)} whole query blocks (64 rows) of the n={n} workload at positions "
+                      f"{[b * 64 for b in bl]}, {sum(t):.1f} s incl. the amortised one-time work; "
+                      "numpy float64 oracle port of select_blocks(approx) + sparse_forward"}
 
 
 # ----------------------------------------------------------------------------- our arm
+
+def _max_over_ranks(ms, ws):
+    import torch
+    import torch.distributed as dist
+    if ws <= 1:
+        return ms
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _timed(step, steps, ws, stream, clk=None):
+    """K steps bracketed by barrier + synchronize, CUDA events on `stream`;
+    returns the max over ranks of ms per step."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk is not None:
+        clk.__enter__()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__(None, None, None)
+    ms = e0.elapsed_time(e1) / steps
+    return _max_over_ranks(ms, ws)
+
+
+def count_launches(step):
+    """Kernels launched by one step, from the CUDA activity trace
+    (torch.profiler / CUPTI): (total, ours, names of ours)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    names = []
+    for e in prof.events():
+        dt = str(getattr(e, "device_type", ""))
+        if "CUDA" in dt and "mem" not in e.name.lower():
+            names.append(e.name)
+    ours = [nm for nm in names if "swattn" in nm]
+    return len(names), len(ours), sorted(set(ours))
+
 
 def run_ours(args):
     import torch
@@ -170,20 +267,21 @@ def run_ours(args):
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    args.cp = args.cp or args.cp_sharded
+    strong = args.cp or args.cp_sharded
     from paper_2509_24663_b200 import _lib
     from paper_2509_24663_b200.core import AttentionConfig, make_qkv
-    from paper_2509_24663_b200.counts import (compress_bytes, dense_total_counts,
-                                              selection_total_counts, sparse_total_counts)
-    from paper_2509_24663_b200.parallel import (context_parallel_attend,
-                                                context_parallel_attend_sharded, shard_rows)
+    from paper_2509_24663_b200.counts import (compress_bytes, selection_total_counts,
+                                              sparse_total_counts)
+    from paper_2509_24663_b200.parallel import (context_parallel_attend_sharded, group_cp_attend,
+                                                group_cp_plan, shard_rows)
     from paper_2509_24663_b200.switch import attend_host_chunked
 
     cfg = AttentionConfig()
     n = args.n
     L = _lib.lib()
     c = _lib.c_config(cfg)
-    Q, K, V = make_qkv(n, 32, 2, 128, seed=0 if args.cp else rank, device="cuda")
+    # weak scaling: rank r serves its own sequence (seed r); strong: one sequence
+    Q, K, V = make_qkv(n, 32, 2, 128, seed=0 if strong else rank, device="cuda")
     O_ = torch.empty_like(Q)
     lse = torch.empty((n, 32), dtype=torch.float32, device="cuda")
     wsb = L.swattn_workspace_bytes(c, n)
@@ -195,37 +293,42 @@ def run_ours(args):
     if args.cp_sharded:
         Q_sh, K_sh, V_sh = (x[a_sh:b_sh].contiguous() for x in (Q, K, V))
 
-    def step():
-        if args.cp_sharded:
-            context_parallel_attend_sharded(Q_sh, K_sh, V_sh, cfg, n)
-            return
-        if args.cp:
-            context_parallel_attend(Q, K, V, cfg, ws, rank, O=O_, lse=lse)
-            return
+    def step_weak():
         _lib.check(L.swattn_attend(c, Q.data_ptr(), K.data_ptr(), V.data_ptr(), n, -1, 0, 2,
                                    O_.data_ptr(), lse.data_ptr(), _lib.ctypes.byref(taken),
                                    work.data_ptr(), wsb, sh), "attend")
 
+    def step_strong():
+        group_cp_attend(Q, K, V, cfg, ws, rank, O=O_, lse=lse, ws=work)
+
+    def step_sharded():
+        context_parallel_attend_sharded(Q_sh, K_sh, V_sh, cfg, n)
+
+    step = step_sharded if args.cp_sharded else step_strong if args.cp else step_weak
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    tokens_per_s = (n if args.cp else ws * n) / (ms / 1e3)
+    clk = ClockSampler(local)
+    ms = _timed(step, args.steps, ws, stream, clk)
+    tokens_per_s = (n if strong else ws * n) / (ms / 1e3)
+
+    # strong scaling of ONE sequence over the same ranks (group x row-range split)
+    strong_line = None
+    if ws > 1 and not strong:
+        Q0, K0, V0 = make_qkv(n, 32, 2, 128, seed=0, device="cuda") if rank != 0 else (Q, K, V)
+
+        def step_s():
+            group_cp_attend(Q0, K0, V0, cfg, ws, rank, O=O_, lse=lse, ws=work)
+        for _ in range(2):
+            step_s()
+        ms_s = _timed(step_s, max(3, min(args.steps, 10)), ws, stream)
+        (g0, g1), (r0, r1) = group_cp_plan(cfg, n, ws, rank)
+        strong_line = {"value": n / (ms_s / 1e3), "unit": "tokens/s", "ms_per_step": ms_s,
+                       "workload": f"one n={n} sequence split over {ws} ranks",
+                       "parallelism": "KV groups x cost-balanced query-row ranges "
+                                      "(swattn_attend_rows_groups), K/V replicated, no data-path "
+                                      "collective",
+                       "rank0_share": {"groups": [g0, g1], "rows": [r0, r1]}}
+        del Q0, K0, V0
 
     # ---- e2e through the public API with host buffers (H2D + D2H in the timed region)
     Qh = Q.cpu().pin_memory()
@@ -235,16 +338,14 @@ def run_ours(args):
     lh = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
 
     def e2e_step_cp():
-        # CP: each rank copies the whole sequence in, computes its rows and
-        # returns only its own O/lse rows
+        # strong: each rank copies the whole sequence in, computes its share and
+        # returns only its own rows of O / lse
         qd, kd, vd = (x.to("cuda", non_blocking=True) for x in (Qh, Kh, Vh))
-        _, _, (r0, r1) = context_parallel_attend(qd, kd, vd, cfg, ws, rank, O=O_, lse=lse)
+        _, _, _, (r0, r1) = group_cp_attend(qd, kd, vd, cfg, ws, rank, O=O_, lse=lse, ws=work)
         Oh[r0:r1].copy_(O_[r0:r1], non_blocking=True)
         lh[r0:r1].copy_(lse[r0:r1], non_blocking=True)
 
     def e2e_step_cp_sharded():
-        # sharded CP: each rank copies in only its rows of Q/K/V and returns
-        # its rows of O/lse (the all-gathers run on the device)
         qd, kd, vd = (x[a_sh:b_sh].to("cuda", non_blocking=True) for x in (Qh, Kh, Vh))
         o_sh, l_sh, _ = context_parallel_attend_sharded(qd, kd, vd, cfg, n)
         Oh[a_sh:b_sh].copy_(o_sh, non_blocking=True)
@@ -262,29 +363,21 @@ def run_ours(args):
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(2):
         e2e_step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / e2e_steps
-    if ws > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = _timed(e2e_step, e2e_steps, ws, stream)
     h2d = (Q.numel() + K.numel() + V.numel()) * 2
     d2h = O_.numel() * 2 + lse.numel() * 4
+
+    # ---- kernels per step (CUPTI activity trace of one extra step)
+    try:
+        total_k, ours_k, our_names = count_launches(step)
+    except Exception as e:  # pragma: no cover - profiler unavailable
+        total_k, ours_k, our_names = None, None, [f"unavailable: {str(e)[:80]}"]
 
     # ---- per-stage breakdown (same stream, CUDA events) for the roofline
     stages = stage_breakdown(L, c, cfg, Q, K, V, n, stream)
     peaks = _peaks()
     sp_mac, _ = sparse_total_counts(cfg, n)
     sel = selection_total_counts(cfg, n, approx=True)
-    dn_mac, _ = dense_total_counts(cfg, n)
     algo = {"K1_compress": ("hbm", compress_bytes(cfg, n)),
             "K2_block_scores": ("tensor", 2 * sel["mac"]),
             "K3_topk": ("hbm", _topk_bytes(cfg, n)),
@@ -300,22 +393,26 @@ def run_ours(args):
     dense = dense_comparator(Q, K, V, cfg, n, stream) if rank == 0 and not args.no_dense else {}
 
     if rank == 0:
+        if args.cp_sharded:
+            par = (f"context parallel, sequence-sharded inputs over {ws} rank(s): NCCL all-gather "
+                   "of the K halo, compressed keys and K/V")
+        elif args.cp:
+            par = (f"one sequence over {ws} rank(s): KV groups x cost-balanced query rows "
+                   "(swattn_attend_rows_groups), K/V replicated, no data-path collective")
+        else:
+            par = (f"batch sharding: {ws} rank(s), one sequence (both KV groups) per rank, "
+                   "no data-path collective")
         line = {
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong" if args.cp else "weak",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (make_qkv Philox normal(0,1), bf16)",
-            "config": {"workload": f"attend (sparse branch) prefill, n={n} tokens, batch 1 per GPU",
-                       "n": n, "batch_per_gpu": 1, "h_q": 32, "h_kv": 2, "d_h": 128, "B": 64,
-                       "budget_blocks": "1+32+63", "selection_mode": "approx",
-                       "parallelism": (f"context parallel, sequence-sharded inputs over {ws} rank(s): "
-                                       f"NCCL all-gather of the K halo, compressed keys and K/V"
-                                       if args.cp_sharded else
-                                       f"context parallel: one sequence, cost-balanced query rows over "
-                                       f"{ws} rank(s), K/V replicated, no data-path collective"
-                                       if args.cp else
-                                       f"batch x kv-group sharding, {ws} rank(s), no collective"),
+            "config": {"workload": f"attend (sparse branch) prefill, n={n} tokens, "
+                                   f"{'one sequence in total' if strong else 'batch 1 per GPU'}",
+                       "n": n, "batch_per_gpu": 0 if strong else 1, "h_q": 32, "h_kv": 2,
+                       "d_h": 128, "B": 64, "budget_blocks": "1+32+63", "selection_mode": "approx",
+                       "parallelism": par,
                        "l2": "inputs larger than L2 (Q = 1 GiB), no flush"},
             "roofline": {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,
@@ -329,33 +426,29 @@ def run_ours(args):
                     "peak": peaks["tflops_sustained"],
                     "frac": part_a_flop(cfg, n) / (stages["K4_part_A_fa_tile"] / 1e3) / 1e12
                     / peaks["tflops_sustained"]},
-                "K4_part_B_sparse_pw (mma.sync, per-token top-k gather)": {
-                    "ms": stages["K4_part_B_sparse_pw_est"], "bound": "L2->SM gather",
-                    "unit": "TB/s",
-                    "achieved": _gather_bytes(cfg, n) / (stages["K4_part_B_sparse_pw_est"] / 1e3) / 1e12,
-                    "peak": 19.7,
-                    "frac": _gather_bytes(cfg, n) / (stages["K4_part_B_sparse_pw_est"] / 1e3) / 1e12 / 19.7,
-                    "peak_source": "per-SM gather ceiling 133 GB/s x 148 (profiles/r01c_gather_sm_sweep.txt)"},
+                "K4_part_B (per-token top-k blocks)": {
+                    "ms": stages["K4_part_B_est"], "bound": "tensor (mma.sync)",
+                    "unit": "TFLOP/s",
+                    "achieved": part_b_flop(cfg, n) / (stages["K4_part_B_est"] / 1e3) / 1e12,
+                    "gather_TBs_per_token_design": _gather_bytes(cfg, n)
+                    / (stages["K4_part_B_est"] / 1e3) / 1e12},
             },
-            "k4_gather": {"bytes": _gather_bytes(cfg, n),
-                          "achieved_TBs_over_K4": _gather_bytes(cfg, n) / (stages["K4_sparse_attention"] / 1e3) / 1e12,
-                          "l2_gather_peak_TBs": 19.7,
-                          "peak_source": "tools/gather_bench.cu SM sweep: 133 GB/s per SM x 148 SMs, "
-                                         "bound per SM (profiles/r01c_gather_sm_sweep.txt)"},
-            "e2e": {"value": ws * n / (e2e_ms / 1e3), "unit": "tokens/s",
+            "e2e": {"value": (n if strong else ws * n) / (e2e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            # per attend: compress, scores_tc, topk, rerank_p1, rerank,
-            # fa_tile (part A), sparse_pw (part B), attention_list (overflow
-            # rows) -- see the committed ncu launch list under profiles/
-            "gpu_launches": args.steps * 8,
+            # counted from the CUPTI trace of one step (count_launches) x steps
+            "gpu_launches": (ours_k * args.steps) if ours_k is not None else None,
+            "launches_per_step": {"ours": ours_k, "all": total_k, "kernels": our_names},
             "dense_comparator": dense,
             "clocks": clk.summary(),
         }
+        if strong_line is not None:
+            line["strong_scaling"] = strong_line
         if dense.get("best"):
-            line["speedup_vs_dense"] = dense["best"]["ms"] / ms
-            line["speedup_vs_dense_impl"] = dense["best"]["impl"]
+            if not strong or ws == 1:   # one sequence per GPU on both sides
+                line["speedup_vs_dense"] = dense["best"]["ms"] / ms
+                line["speedup_vs_dense_impl"] = dense["best"]["impl"]
         if not args.no_cpu and ws == 1:
-            line["cpu_baseline"] = cpu_baseline_sample(n, rows_n=args.cpu_rows)
+            line["cpu_baseline"] = cpu_baseline_sample(n, blocks=args.cpu_blocks)
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()
@@ -445,7 +538,7 @@ def stage_breakdown(L, c, cfg, Q, K, V, n, stream, reps=2):
         out[name] = a.elapsed_time(b) / reps
     out["rerank_est"] = max(0.0, out["select_total"] - out["K1_compress"] - out["K2_block_scores"]
                             - out["K3_topk"])
-    out["K4_part_B_sparse_pw_est"] = max(0.0, out["K4_sparse_attention"] - out["K4_part_A_fa_tile"])
+    out["K4_part_B_est"] = max(0.0, out["K4_sparse_attention"] - out["K4_part_A_fa_tile"])
     return out
 
 
@@ -457,6 +550,12 @@ def part_a_flop(cfg, n):
     picked = np.minimum(b + 1, cfg.N_init + cfg.N_local)
     vis = int(((picked - 1) * cfg.B + (i - b * cfg.B) + 1).sum())
     return 4 * cfg.h_q * vis * cfg.d_h
+
+
+def part_b_flop(cfg, n):
+    """Algorithmic FLOPs of K4 part B: every token's top-k keys."""
+    from paper_2509_24663_b200.counts import sparse_total_counts
+    return 2 * sparse_total_counts(cfg, n)[0] - part_a_flop(cfg, n)
 
 
 def dense_comparator(Q, K, V, cfg, n, stream, reps=3):
@@ -489,12 +588,25 @@ def dense_comparator(Q, K, V, cfg, n, stream, reps=3):
         with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
             return F.scaled_dot_product_attention(q, k, v, is_causal=True)
     cands["torch SDPA cuDNN"] = cudnn
+    fi = _flashinfer_trtllm(Q, K, V, n)
+    if fi is not None:
+        cands["flashinfer 0.6.11 trtllm-gen FMHA (sm100 cubin, paged 64)"] = fi
     mac, _ = dense_total_counts(cfg, n)
     out = {}
     for name, fn in cands.items():
         try:
-            fn()
+            o = fn()
             torch.cuda.synchronize()
+            if name.startswith("flashinfer"):
+                # the comparator must compute the same attention: check rows
+                # against our K5 output (dense O_ from the own-K5 run above)
+                _lib.check(L.swattn_dense_fwd(c, Q.data_ptr(), K.data_ptr(), V.data_ptr(), n, 1,
+                                              O_.data_ptr(), lse.data_ptr(), stream.cuda_stream),
+                           "dense")
+                rows = torch.tensor([0, 1, 777, n // 2, n - 1], device="cuda")
+                err = float((o[rows].float() - O_[rows].float()).abs().max())
+                if not err < 5e-2:
+                    raise RuntimeError(f"output mismatch vs K5: max-abs {err}")
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for _ in range(reps):
@@ -513,6 +625,32 @@ def dense_comparator(Q, K, V, cfg, n, stream, reps=3):
     return out
 
 
+def _flashinfer_trtllm(Q, K, V, n, page=64):
+    """flashinfer's trtllm-gen FMHA (prebuilt sm100 cubins: no JIT) as a dense
+    causal comparator over a paged view of the same K / V.  None if absent."""
+    try:
+        import torch
+        from flashinfer.prefill import trtllm_batch_context_with_kv_cache
+    except Exception:
+        return None
+    nb = -(-n // page)
+    pad = nb * page - n
+    def pages(x):
+        x = torch.nn.functional.pad(x, (0, 0, 0, 0, 0, pad)) if pad else x
+        return x.view(nb, page, x.shape[1], x.shape[2]).permute(0, 2, 1, 3).contiguous()
+    kc, vc = pages(K), pages(V)
+    wsb = torch.zeros(512 << 20, dtype=torch.uint8, device="cuda")
+    bt = torch.arange(nb, dtype=torch.int32, device="cuda")[None]
+    seq = torch.tensor([n], dtype=torch.int32, device="cuda")
+    cu = torch.tensor([0, n], dtype=torch.int32, device="cuda")
+    scale = 1.0 / float(Q.shape[2]) ** 0.5
+
+    def run():
+        return trtllm_batch_context_with_kv_cache(Q, (kc, vc), wsb, bt, seq, n, n, scale, 1.0, 1,
+                                                  cu, cu, kv_layout="HND")
+    return run
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -520,7 +658,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--n", type=int, default=131072)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-rows", type=int, default=48)
+    ap.add_argument("--cpu-blocks", type=int, default=4,
+                    help="query blocks of the CPU port timed for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cp", action="store_true",
@@ -532,6 +671,17 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torch.distributed.run
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -137,6 +137,19 @@ int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K
                           size_t workspace_bytes, void *stream);
 size_t swattn_sparse_workspace_bytes(const swattn_config *cfg, int64_t n);
 
+/* K4, general form -- sparse_forward (sparse.py:43-98) over an ARBITRARY
+ * BlockSelection (selection.py:51-66: any sorted block ids per (group, row),
+ * e.g. load_selection(path) fixtures, selection.py:403-430, or every causal
+ * block, bench.py:207-210).  blocks [h_kv, n, ld] int32, row (g, i) lists
+ * cnt[g, i] block ids in visiting order (ascending in a BlockSelection);
+ * negative ids are ignored.  Block j covers keys [j B, min(j B + B, n, i + 1))
+ * (selection.py:73-87).  A row with no visible key gets O = 0, lse = -inf
+ * (the reference raises RuntimeError, sparse.py:75-76: callers check first).
+ * Needs G = 16, d_h = 128; any B. */
+int32_t swattn_sparse_fwd_lists(const swattn_config *cfg, const void *Q, const void *K,
+                                const void *V, int64_t n, const int32_t *blocks, int64_t ld,
+                                const int32_t *cnt, void *O, float *lse, void *stream);
+
 /* K5 -- tiled_gqa_forward (dense.py:112-170): causal (or full) GQA flash
  * attention, O bf16, lse fp32. */
 int32_t swattn_dense_fwd(const swattn_config *cfg, const void *Q, const void *K,
@@ -205,6 +218,23 @@ int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *
                            const void *V, int64_t n, int64_t r0, int64_t r1,
                            int32_t select_mode, void *O, float *lse, void *workspace,
                            size_t workspace_bytes, void *stream);
+
+/* ---- batch x KV-group sharding ----
+ * The same calls restricted to KV groups [g0, g1): query heads
+ * [g0 G, g1 G) and K/V heads [g0, g1) of the full tensors (G = h_q / h_kv);
+ * only those heads' O / lse rows are written.  Groups are independent end to
+ * end (selection.py:111-135, sparse.py:70-91), so rank r of a group-sharded
+ * job calls these with its own groups and needs no collective.  The
+ * workspace is sized as for the full call (swattn_workspace_bytes). */
+int32_t swattn_attend_groups(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                             int64_t n, int32_t g0, int32_t g1, int64_t threshold,
+                             int32_t forced_mode, int32_t select_mode, void *O, float *lse,
+                             int32_t *mode_taken, void *workspace, size_t workspace_bytes,
+                             void *stream);
+int32_t swattn_attend_rows_groups(const swattn_config *cfg, const void *Q, const void *K,
+                                  const void *V, int64_t n, int64_t r0, int64_t r1, int32_t g0,
+                                  int32_t g1, int32_t select_mode, void *O, float *lse,
+                                  void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---- decode over a paged KV cache (K6; semantics = last row of attend) ----
  * Paged layout: page = B tokens; k_pages/v_pages [num_pages, B, h_kv, d_h]

@@ -180,14 +180,21 @@ def shared_scores(Q, K, cfg: Profile, mode: str = "approx", rows=None, chunk: in
     for c0 in range(0, rows.size, chunk):
         r = rows[c0:c0 + chunk]
         v1 = vis1[c0:c0 + chunk]
+        # columns no row of the chunk sees are skipped (the reference's tile
+        # loops stop at the first future tile, selection.py:178-179,211-212);
+        # they stay 0 in `out` exactly as masked columns do
+        c1 = int(v1.max()) if v1.size else 0
+        if c1 == 0:
+            continue
         Qr = Q[r].astype(np.float64)
         for g in range(cfg.h_kv):
             Qg = Qr[:, g * G:(g + 1) * G]
-            S1 = _logits(Qg, K1[:, g], scale)
+            S1 = _logits(Qg, K1[:c1, g], scale)
             if mode == "approx":
                 v2 = vis2[c0:c0 + chunk]
-                if K2.shape[0]:
-                    lse = _masked_lse(_logits(Qg, K2[:, g], scale), v2)
+                c2 = int(v2.max()) if v2.size else 0
+                if K2.shape[0] and c2 > 0:
+                    lse = _masked_lse(_logits(Qg, K2[:c2, g], scale), v2)
                 else:
                     lse = np.full(S1.shape[:2], -np.inf)
                 fb = (v2 == 0) & (v1 > 0)
@@ -197,8 +204,8 @@ def shared_scores(Q, K, cfg: Profile, mode: str = "approx", rows=None, chunk: in
                 lse = _masked_lse(S1, v1)
             lse_safe = np.where(np.isneginf(lse), 0.0, lse)
             P = np.exp(S1 - lse_safe[..., None])
-            P = np.where(np.arange(m1)[None, None, :] < v1[:, None, None], P, 0.0)
-            out[c0:c0 + chunk, g] = P.sum(axis=1)
+            P = np.where(np.arange(c1)[None, None, :] < v1[:, None, None], P, 0.0)
+            out[c0:c0 + chunk, g, :c1] = P.sum(axis=1)
     return out, no_visible
 
 
@@ -260,12 +267,13 @@ def full_block_set(topk_row: np.ndarray, i: int, cfg: Profile) -> np.ndarray:
     return np.union1d(base, t).astype(np.int64)
 
 
-def select(Q, K, cfg: Profile, mode: str = "approx", rows=None):
+def select(Q, K, cfg: Profile, mode: str = "approx", rows=None, ck1=None, ck2=None):
     """select_blocks pipeline restated (selection.py:354-383): pool, score,
-    max-pool, top-k.  Returns (topk, counts, scmp) for the given rows."""
+    max-pool, top-k.  Returns (topk, counts, scmp) for the given rows.
+    ck1 / ck2: the pooled keys when the caller already has them."""
     n = Q.shape[0]
     rows = np.arange(n) if rows is None else np.asarray(rows, dtype=np.int64)
-    S, nv = shared_scores(Q, K, cfg, mode=mode, rows=rows)
+    S, nv = shared_scores(Q, K, cfg, mode=mode, rows=rows, ck1=ck1, ck2=ck2)
     scmp = block_scores(S, cfg.l, cfg.s)
     top, counts = topk_blocks(scmp, nv, rows, n, cfg)
     return top, counts, scmp
@@ -282,6 +290,13 @@ def token_mask_row(i: int, blocks: np.ndarray, n: int, B: int) -> np.ndarray:
     return m
 
 
+def visible_keys(i: int, blocks: np.ndarray, n: int, B: int) -> np.ndarray:
+    """Ascending key ids of token_mask_row (blocks ascending and disjoint)."""
+    parts = [np.arange(j * B, min(j * B + B, n, i + 1)) for j in blocks]
+    parts = [p for p in parts if p.size]
+    return np.concatenate(parts) if parts else np.empty(0, dtype=np.int64)
+
+
 def sparse_attention(Q, K, V, topk: np.ndarray, cfg: Profile, rows=None, out_dtype=None):
     """Exact masked softmax over each row's visible set, float64
     (sparse.py:43-98, oracle form sparse.py:101-127).  topk is
@@ -291,14 +306,14 @@ def sparse_attention(Q, K, V, topk: np.ndarray, cfg: Profile, rows=None, out_dty
     rows = np.arange(n) if rows is None else np.asarray(rows, dtype=np.int64)
     G = cfg.G
     scale = 1.0 / np.sqrt(cfg.d_h)
-    K64 = K.astype(np.float64)
-    V64 = V.astype(np.float64)
+    K64 = K.astype(np.float64, copy=False)
+    V64 = V.astype(np.float64, copy=False)
     O = np.empty((rows.size, cfg.h_q, cfg.d_h))
     L = np.empty((rows.size, cfg.h_q))
     for ri, i in enumerate(rows):
         for g in range(cfg.h_kv):
             blocks = full_block_set(topk[g, i], int(i), cfg)
-            keys = np.flatnonzero(token_mask_row(int(i), blocks, n, cfg.B))
+            keys = visible_keys(int(i), blocks, n, cfg.B)
             if keys.size == 0:
                 raise RuntimeError(f"query {i} in group {g} has an empty visible set")
             q = Q[i, g * G:(g + 1) * G].astype(np.float64)
@@ -431,8 +446,18 @@ def decode_row(q_row, K, V, t: int, cfg: Profile):
     q_row [h_q, d]; K, V [>= t+1, h_kv, d].  Returns (O [h_q, d], lse [h_q],
     topk [h_kv, k_top])."""
     n = t + 1
-    Q = np.zeros((n, cfg.h_q, cfg.d_h), dtype=K.dtype)
-    Q[t] = q_row
+
+    class _OneRow:   # Q of n rows of which only row t is ever read
+        shape = (n, cfg.h_q, cfg.d_h)
+
+        def __getitem__(self, idx):
+            if isinstance(idx, tuple):
+                assert int(idx[0]) == t
+                return q_row[idx[1:]]
+            r = np.asarray(idx)
+            assert np.all(r == t)
+            return np.broadcast_to(q_row, r.shape + q_row.shape)
+    Q = _OneRow()
     Kn, Vn = K[:n], V[:n]
     top, _, _ = select(Q, Kn, cfg, mode="approx", rows=np.array([t]))
     full = np.full((cfg.h_kv, n, cfg.k_top), -1, dtype=np.int64)

@@ -80,6 +80,7 @@ def lib():
         "swattn_select_blocks": (I32, [cfgp, P, P, I64, I32, P, P, P, P, SZ, P]),
         "swattn_sparse_fwd": (I32, [cfgp, P, P, P, I64, P, P, P, P, P, SZ, P]),
         "swattn_sparse_workspace_bytes": (SZ, [cfgp, I64]),
+        "swattn_sparse_fwd_lists": (I32, [cfgp, P, P, P, I64, P, I64, P, P, P, P]),
         "swattn_sparse_bwd": (I32, [cfgp, P, P, P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
         "swattn_sparse_bwd_workspace_bytes": (SZ, [cfgp, I64]),
         "swattn_dense_bwd": (I32, [cfgp, P, P, P, I64, I32, P, P, P, P, P, P, P, SZ, P]),
@@ -91,6 +92,10 @@ def lib():
         "swattn_sparse_fwd_rows": (I32, [cfgp, P, P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
         "swattn_attend_rows": (I32, [cfgp, P, P, P, I64, I64, I64, I32, P, P, P, SZ, P]),
         "swattn_attend_prepare": (I32, [cfgp, P, I64, P, SZ, P]),
+        "swattn_attend_groups": (I32, [cfgp, P, P, P, I64, I32, I32, I64, I32, I32, P, P,
+                                       ctypes.POINTER(I32), P, SZ, P]),
+        "swattn_attend_rows_groups": (I32, [cfgp, P, P, P, I64, I64, I64, I32, I32, I32, P, P, P,
+                                            SZ, P]),
         "swattn_workspace_ckeys": (I32, [cfgp, I64, P, ctypes.POINTER(P), ctypes.POINTER(P)]),
         "swattn_kcache_append": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P]),
         "swattn_decode_step": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P, P, P, P, SZ, P]),
@@ -108,10 +113,10 @@ EXPORTED = (
     "swattn_last_error", "swattn_version", "swattn_validate_config", "swattn_profile_supported",
     "swattn_num_pooled", "swattn_workspace_bytes", "swattn_compress_keys", "swattn_block_scores",
     "swattn_shared_scores", "swattn_topk_blocks", "swattn_select_blocks", "swattn_sparse_fwd",
-    "swattn_sparse_workspace_bytes", "swattn_sparse_bwd", "swattn_sparse_bwd_workspace_bytes",
+    "swattn_sparse_workspace_bytes", "swattn_sparse_fwd_lists", "swattn_sparse_bwd", "swattn_sparse_bwd_workspace_bytes",
     "swattn_dense_bwd", "swattn_dense_bwd_workspace_bytes",
     "swattn_dense_fwd", "swattn_attend", "swattn_select_blocks_rows", "swattn_sparse_fwd_rows",
-    "swattn_attend_rows", "swattn_attend_prepare", "swattn_workspace_ckeys", "swattn_kcache_append", "swattn_decode_step",
+    "swattn_attend_rows", "swattn_attend_prepare", "swattn_attend_groups", "swattn_attend_rows_groups", "swattn_workspace_ckeys", "swattn_kcache_append", "swattn_decode_step",
     "swattn_decode_workspace_bytes",
 )
 

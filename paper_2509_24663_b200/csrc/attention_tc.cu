@@ -49,7 +49,7 @@ struct FaParams {
   CUtensorMap k_map;   // K [n][h_kv*d]: box {64, 64}
   CUtensorMap v_map;
   int64_t n;
-  int h_q, h_kv;
+  int h_q, h_kv, g0, gc;
   int n_tiles;         // token tiles of 8 in this launch
   int tile_end;        // tiles [tile_end - n_tiles, tile_end)
   int mode;            // 0 dense causal, 1 dense non-causal, 2 sparse part A
@@ -116,7 +116,7 @@ __device__ __forceinline__ int64_t fa_slot_item(int64_t w, int64_t n_items) {
 __device__ __forceinline__ void fa_item(const FaParams &p, int64_t w, int &tile, int &g) {
   // group-major (one group's K/V, 67 MB at 128K, stays L2-resident while its
   // tiles run), heavy (late) tiles first within a group
-  g = (int)(w / p.n_tiles);
+  g = p.g0 + (int)(w / p.n_tiles);
   tile = p.tile_end - 1 - (int)(w % p.n_tiles);
 }
 
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
   FaSmem &s = *reinterpret_cast<FaSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nb_total = cdiv(p.n, kBlk);
-  const int64_t n_items = (int64_t)p.n_tiles * p.h_kv;
+  const int64_t n_items = (int64_t)p.n_tiles * p.gc;
 
   if (threadIdx.x == 0) {
     tc::mbar_init(&s.q_full, 1);
@@ -425,6 +425,9 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   p.n = n;
   p.h_q = cfg->h_q;
   p.h_kv = cfg->h_kv;
+  const GroupRange gr = group_range(cfg);
+  p.g0 = gr.g0;
+  p.gc = gr.gc;
   // row ranges are multiples of the 8-token tile (the last one may end at n)
   p.tile_end = (int)cdiv(r1, kTokTile);
   p.n_tiles = p.tile_end - (int)(r0 / kTokTile);
@@ -456,7 +459,7 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   // 4K dense 0.205 -> 0.146 ms, 32K 11.0 -> 8.1 ms); above it one CTA per
   // item lets the block scheduler balance the long causal rows (128K dense:
   // 119 ms one-per-item vs 145 ms persistent).
-  const int64_t items = (int64_t)p.n_tiles * cfg->h_kv;
+  const int64_t items = (int64_t)p.n_tiles * gr.gc;
 #ifndef SWATTN_FA_PERSIST_ITEMS
 #define SWATTN_FA_PERSIST_ITEMS 8192
 #endif

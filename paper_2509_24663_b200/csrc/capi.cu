@@ -14,6 +14,20 @@
 namespace swattn {
 
 static thread_local char g_err[512] = "";
+static thread_local int g_group0 = 0, g_group1 = -1;  // -1: all groups
+
+GroupRange group_range(const swattn_config *cfg) {
+  if (g_group1 < 0) return GroupRange{0, cfg->h_kv};
+  return GroupRange{g_group0, g_group1 - g_group0};
+}
+GroupScope::GroupScope(int g0, int g1) : prev_g0(g_group0), prev_g1(g_group1) {
+  g_group0 = g0;
+  g_group1 = g1;
+}
+GroupScope::~GroupScope() {
+  g_group0 = prev_g0;
+  g_group1 = prev_g1;
+}
 
 void set_error(const char *fmt, ...) {
   va_list ap;
@@ -57,6 +71,9 @@ int32_t launch_sparse_part_b(const swattn_config *, const void *, const void *, 
                              const float *,
                              const float *, void *, float *, int32_t *, int32_t *, int,
                              cudaStream_t);
+int32_t launch_sparse_list(const swattn_config *, const void *, const void *, const void *, int64_t,
+                           const int32_t *, int64_t, const int32_t *, void *, float *, int,
+                           cudaStream_t);
 int32_t launch_attention_list(const swattn_config *, const void *, const void *, const void *,
                               int64_t, const int32_t *, const int32_t *, const int32_t *,
                               const int32_t *, void *, float *, int, cudaStream_t);
@@ -80,17 +97,12 @@ static int num_sms() {
   return sms;
 }
 
-// SWATTN_FORCE_SIMT=1 routes K2/K4/K5 to the CUDA-core kernels (A/B checks).
-static bool use_tc_scores() {
-  static int v = -1;
-  if (v < 0) v = getenv("SWATTN_FORCE_SIMT") == nullptr;
-  return v && scores_tc_available();
-}
-static bool use_tc_attention() {
-  static int v = -1;
-  if (v < 0) v = getenv("SWATTN_FORCE_SIMT") == nullptr;
-  return v && attention_tc_available();
-}
+// The tensor-core kernels are the only path for the paper profile; the
+// CUDA-core kernels (scores_simt.cu / attention_simt.cu) serve the profiles
+// the tcgen05 tiles are not compiled for (e.g. the reference's small
+// check profile, bench.py:199-204).  No run-time switch between the two.
+static bool use_tc_scores() { return scores_tc_available(); }
+static bool use_tc_attention() { return attention_tc_available(); }
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -312,9 +324,9 @@ static int32_t check_rows(const swattn_config *cfg, int64_t n, int64_t r0, int64
   return SWATTN_OK;
 }
 
-static int32_t memset_rows(void *base, int64_t n, int h_kv, int64_t r0, int64_t r1, size_t row_bytes,
-                           int value, cudaStream_t st) {
-  for (int g = 0; g < h_kv; ++g) {
+static int32_t memset_rows(void *base, int64_t n, GroupRange gr, int64_t r0, int64_t r1,
+                           size_t row_bytes, int value, cudaStream_t st) {
+  for (int g = gr.g0; g < gr.g0 + gr.gc; ++g) {
     char *p = static_cast<char *>(base) + ((size_t)g * n + r0) * row_bytes;
     int32_t rc = cuda_check(cudaMemsetAsync(p, value, (size_t)(r1 - r0) * row_bytes, st), "memset(rows)");
     if (rc) return rc;
@@ -359,15 +371,15 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
   if (r0 == 0 && !prepared && (rc = launch_compress(cfg, K, n, kc1, kc2, st))) return rc;
   if (cfg->k_top == 0 || L.n_cols <= cfg->N_init) {
     if (cfg->k_top > 0 &&
-        (rc = memset_rows(topk, n, cfg->h_kv, r0, r1, (size_t)cfg->k_top * 4, 0xff, st)))
+        (rc = memset_rows(topk, n, group_range(cfg), r0, r1, (size_t)cfg->k_top * 4, 0xff, st)))
       return rc;
-    if ((rc = memset_rows(topk_cnt, n, cfg->h_kv, r0, r1, 4, 0, st))) return rc;
+    if ((rc = memset_rows(topk_cnt, n, group_range(cfg), r0, r1, 4, 0, st))) return rc;
     if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
     return SWATTN_OK;
   }
   if (L.generic || !use_tc_scores()) {
-    if (!full) {
-      set_error("row ranges need the paper profile on the tensor-core path");
+    if (!full || group_range(cfg).gc != cfg->h_kv) {
+      set_error("row ranges and group ranges need the paper profile on the tensor-core path");
       return SWATTN_EUNSUPPORTED;
     }
   }
@@ -507,8 +519,8 @@ static int32_t sparse_rows_impl(const swattn_config *cfg, const void *Q, const v
     return launch_attention_list(cfg, Q, K, V, n, topk, topk_cnt, slow_count, slow_list, O, lse,
                                  num_sms(), st);
   }
-  if (r0 != 0 || r1 != n) {
-    set_error("row ranges need the paper profile on the tensor-core path");
+  if (r0 != 0 || r1 != n || group_range(cfg).gc != cfg->h_kv) {
+    set_error("row ranges and group ranges need the paper profile on the tensor-core path");
     return SWATTN_EUNSUPPORTED;
   }
   return launch_attention_simt(cfg, Q, K, V, n, topk, topk_cnt, 1, 1, O, lse, nullptr, st);
@@ -576,6 +588,32 @@ int32_t swattn_sparse_fwd(const swattn_config *cfg, const void *Q, const void *K
                           float *lse, void *workspace, size_t workspace_bytes, void *stream) {
   return sparse_rows(cfg, Q, K, V, n, 0, n, topk, topk_cnt, O, lse, workspace, workspace_bytes,
                      static_cast<cudaStream_t>(stream));
+}
+
+int32_t swattn_sparse_fwd_lists(const swattn_config *cfg, const void *Q, const void *K,
+                                const void *V, int64_t n, const int32_t *blocks, int64_t ld,
+                                const int32_t *cnt, void *O, float *lse, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1) {
+    set_error("empty sequence: n must be >= 1");
+    return SWATTN_EINVAL;
+  }
+  if (cfg->h_q != kG * cfg->h_kv || cfg->d_h != kD) {
+    set_error("unsupported profile for the attention kernels (need G=16, d_h=128)");
+    return SWATTN_EUNSUPPORTED;
+  }
+  if (ld < 1 || (rc = check_ptr(blocks, "blocks")) || (rc = check_ptr(cnt, "cnt")) ||
+      (rc = check_ptr(Q, "Q")) || (rc = check_ptr(K, "K")) || (rc = check_ptr(V, "V")) ||
+      (rc = check_ptr(O, "O")) || (rc = check_ptr(lse, "lse"))) {
+    if (!rc) {
+      set_error("ld=%lld must be >= 1", (long long)ld);
+      rc = SWATTN_EINVAL;
+    }
+    return rc;
+  }
+  return launch_sparse_list(cfg, Q, K, V, n, blocks, ld, cnt, O, lse, num_sms(),
+                            static_cast<cudaStream_t>(stream));
 }
 
 int32_t swattn_sparse_fwd_rows(const swattn_config *cfg, const void *Q, const void *K,
@@ -652,6 +690,10 @@ int32_t swattn_dense_fwd(const swattn_config *cfg, const void *Q, const void *K,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (use_tc_attention())
     return launch_dense_tc(cfg, Q, K, V, n, causal, O, lse, st);
+  if (group_range(cfg).gc != cfg->h_kv) {
+    set_error("group ranges need the tensor-core attention kernels");
+    return SWATTN_EUNSUPPORTED;
+  }
   return launch_attention_simt(cfg, Q, K, V, n, nullptr, nullptr, 0, causal, O, lse, nullptr, st);
 }
 
@@ -739,6 +781,37 @@ int32_t swattn_attend_rows(const swattn_config *cfg, const void *Q, const void *
               align_up((size_t)cfg->h_kv * n * 4);
   return select_and_sparse(cfg, Q, K, V, n, r0, r1, select_mode, topk, cnt, O, lse, workspace,
                            L.total, sws, swattn_sparse_workspace_bytes(cfg, n), st);
+}
+
+static int32_t check_groups(const swattn_config *cfg, int32_t g0, int32_t g1) {
+  if (g0 < 0 || g1 > cfg->h_kv || g0 >= g1) {
+    set_error("group range [%d, %d) must satisfy 0 <= g0 < g1 <= h_kv=%d", g0, g1, cfg->h_kv);
+    return SWATTN_EINVAL;
+  }
+  return SWATTN_OK;
+}
+
+int32_t swattn_attend_groups(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                             int64_t n, int32_t g0, int32_t g1, int64_t threshold,
+                             int32_t forced_mode, int32_t select_mode, void *O, float *lse,
+                             int32_t *mode_taken, void *workspace, size_t workspace_bytes,
+                             void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc || (rc = check_groups(cfg, g0, g1))) return rc;
+  GroupScope scope(g0, g1);
+  return swattn_attend(cfg, Q, K, V, n, threshold, forced_mode, select_mode, O, lse, mode_taken,
+                       workspace, workspace_bytes, stream);
+}
+
+int32_t swattn_attend_rows_groups(const swattn_config *cfg, const void *Q, const void *K,
+                                  const void *V, int64_t n, int64_t r0, int64_t r1, int32_t g0,
+                                  int32_t g1, int32_t select_mode, void *O, float *lse,
+                                  void *workspace, size_t workspace_bytes, void *stream) {
+  int32_t rc = swattn_validate_config(cfg);
+  if (rc || (rc = check_groups(cfg, g0, g1))) return rc;
+  GroupScope scope(g0, g1);
+  return swattn_attend_rows(cfg, Q, K, V, n, r0, r1, select_mode, O, lse, workspace,
+                            workspace_bytes, stream);
 }
 
 }  // extern "C"

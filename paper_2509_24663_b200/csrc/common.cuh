@@ -30,6 +30,22 @@ constexpr int kPoolL = 5;   // max-pool window (C1 columns)
 constexpr int kPoolS = 4;   // max-pool stride
 constexpr int kTopMax = 128;  // compiled bound on k_top
 
+// KV-group range of the current C-ABI call (batch x KV-group sharding: a rank
+// computes groups [g0, g0 + gc) only -- query heads [G g0, G (g0 + gc)) and
+// K/V heads [g0, g0 + gc) -- with no collective, selection.py:111-135 and
+// sparse.py:70-91 being independent per group).  {0, h_kv} unless a
+// swattn_*_groups entry point narrowed it for the duration of its call
+// (thread-local, set and restored by GroupScope).
+struct GroupRange {
+  int g0, gc;
+};
+GroupRange group_range(const swattn_config *cfg);
+struct GroupScope {
+  GroupScope(int g0, int g1);
+  ~GroupScope();
+  int prev_g0, prev_g1;
+};
+
 struct Dims {
   int64_t n;
   int h_q, h_kv, d;

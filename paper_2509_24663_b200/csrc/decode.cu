@@ -372,7 +372,8 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
   const int lo = max(0, b - a.N_local + 1);
   const int lo2 = max(lo, n_init);
   const int ntop = topk_cnt[row];
-  const int nvis = n_init + ntop + (b + 1 - lo2);
+  // an empty slot (no cached token) has no visible block: no page is read
+  const int nvis = L < 1 ? 0 : n_init + ntop + (b + 1 - lo2);
   const int32_t *top = topk + (int64_t)row * a.k_top;
   const int vb0 = split * kAttnBlocks, vb1 = min(nvis, vb0 + kAttnBlocks);
   const int64_t pi_base = ((int64_t)row * splits + split) * kG;
@@ -515,6 +516,14 @@ __global__ void __launch_bounds__(512) decode_combine_kernel(DecodeArgs a, const
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
   const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t L = a.seq_lens[seq];
+  if (L < 1) {  // empty slot: defined outputs (O = 0, lse = -inf), nothing read
+    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 0] = __float2bfloat16_rn(0.f);
+    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 1] = __float2bfloat16_rn(0.f);
+    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 2] = __float2bfloat16_rn(0.f);
+    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 3] = __float2bfloat16_rn(0.f);
+    if (lane == 0) lse[(int64_t)seq * a.h_q + g * kG + h] = -INFINITY;
+    return;
+  }
   const int b = (int)((L - 1) / kB);
   const int n_init = min(a.N_init, b + 1);
   const int lo2 = max(max(0, b - a.N_local + 1), n_init);

@@ -68,7 +68,7 @@ struct ScParams {
   CUtensorMap k1_map;   // K_C1 [m1][h_kv*d]: box {64, 128}
   CUtensorMap k2_map;   // K_C2 (or K_C1 again in exact mode)
   int64_t n, m1, m2;
-  int h_q, h_kv;
+  int h_q, h_kv, g0;
   int l_C1, s_C1, l_C2, s_C2;
   int N_init, N_local, B, n_cols;
   int approx;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heavy CTAs (late tokens) first
   const int tt = p.n_tiles_tok - 1 - (int)blockIdx.x;
-  const int g = blockIdx.y;
+  const int g = p.g0 + (int)blockIdx.y;
   const int64_t i0 = p.tok0 + (int64_t)tt * kTok;
   const int64_t i_last = min(i0 + kTok - 1, p.r1 - 1);
   const int b = (int)(i0 / p.B);
@@ -395,7 +395,9 @@ int32_t launch_scores_tc(const swattn_config *cfg, const void *Q, const void *kc
     cudaFuncSetAttribute(scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dim3 grid((unsigned)p.n_tiles_tok, (unsigned)cfg->h_kv);
+  const GroupRange gr = group_range(cfg);
+  p.g0 = gr.g0;
+  dim3 grid((unsigned)p.n_tiles_tok, (unsigned)gr.gc);
   scores_tc_kernel<<<grid, kThreads, smem, stream>>>(p);
   SWATTN_LAUNCH_CHECK("scores_tc_kernel");
   return SWATTN_OK;

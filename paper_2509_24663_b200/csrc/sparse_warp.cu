@@ -74,7 +74,7 @@ struct PwParams {
   CUtensorMap k_map;  // K as (d lo/hi 64, token, half, group): box {64, 16, 2, 1}
   CUtensorMap v_map;
   int64_t n;
-  int h_q, h_kv, k_top;
+  int h_q, h_kv, k_top, g0;
   int64_t tok0, tok1;  // tokens [tok0, tok1) of this launch (all have top-k blocks)
   int64_t n_items;     // h_kv * (tok1 - tok0)
   const int32_t *topk, *topk_cnt;
@@ -101,7 +101,7 @@ struct __align__(1024) PwSmem {
 
 __device__ __forceinline__ void item_of(const PwParams &p, int64_t it, int &g, int64_t &t) {
   const int64_t per = p.tok1 - p.tok0;
-  g = (int)(it / per);
+  g = p.g0 + (int)(it / per);
   t = p.tok0 + it % per;
 }
 
@@ -398,7 +398,9 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
   if (p.tok0 < r0) p.tok0 = r0;
   p.tok1 = r1;
   if (p.tok0 >= r1 || cfg->k_top == 0) return SWATTN_OK;
-  p.n_items = (int64_t)cfg->h_kv * (r1 - p.tok0);
+  const GroupRange gr = group_range(cfg);
+  p.g0 = gr.g0;
+  p.n_items = (int64_t)gr.gc * (r1 - p.tok0);
   p.topk = topk;
   p.topk_cnt = topk_cnt;
   p.m_a = m_a;

@@ -479,7 +479,7 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
 template <bool kReg>
 __global__ void __launch_bounds__(kWarps * 32)
 topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int64_t r0, int64_t r1, int h_kv,
-            int B, int N_init, int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
+            int g0, int B, int N_init, int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
             int32_t *__restrict__ topk, int32_t *__restrict__ topk_cnt, AmbList amb) {
   extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride] (staged path)
   __shared__ int hist_s[kWarps * 256];
@@ -489,7 +489,7 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int64_t r0, 
   const int64_t local = (int64_t)blockIdx.x * kWarps + warp;  // g * per + (i - r0)
   if (local >= (int64_t)h_kv * per) return;
   const int64_t i = r0 + local % per;
-  const int64_t row = (local / per) * n + i;  // g * n + i
+  const int64_t row = (g0 + local / per) * n + i;  // g * n + i
   const int b = (int)(i / B);
   const int hi = cand_hi(b, N_local, n_cols);
   const int ncand = hi > N_init ? hi - N_init : 0;
@@ -562,20 +562,21 @@ int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, in
   }
   if (cfg->k_top <= 0) return SWATTN_OK;
   if (r1 <= r0) return SWATTN_OK;
-  const int64_t rows = (int64_t)cfg->h_kv * (r1 - r0);
+  const GroupRange gr = group_range(cfg);
+  const int64_t rows = (int64_t)gr.gc * (r1 - r0);
   AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
   const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
   const unsigned grid = (unsigned)cdiv(rows, kWarps);
   if (reg_path_ok(s_cmp, ld, cfg->k_top, n_cols)) {
     topk_kernel<true><<<grid, kWarps * 32, 0, stream>>>(
-        s_cmp, ld, n, r0, r1, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols,
+        s_cmp, ld, n, r0, r1, gr.gc, gr.g0, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols,
         cfg->l_C1, cand_stride, topk, topk_cnt, amb);
   } else {
     const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
     if (smem > 40 * 1024)
       cudaFuncSetAttribute(topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     topk_kernel<false><<<grid, kWarps * 32, smem, stream>>>(
-        s_cmp, ld, n, r0, r1, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols,
+        s_cmp, ld, n, r0, r1, gr.gc, gr.g0, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols,
         cfg->l_C1, cand_stride, topk, topk_cnt, amb);
   }
   SWATTN_LAUNCH_CHECK("topk_kernel");

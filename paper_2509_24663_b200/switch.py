@@ -59,7 +59,9 @@ def attend(Q, K, V, cfg: AttentionConfig, policy: SwitchPolicy | None = None,
     if selection_mode not in _lib.SELECT_MODE:
         raise ValueError(f"unknown selection mode {selection_mode!r}")
     host = is_host(Q)
-    if host and mode == MODE_SPARSE and cfg.h_q == 16 * cfg.h_kv and d_h == 128:
+    # the chunked host pipeline needs the row-range entry points, i.e. the
+    # paper profile on the tensor-core kernels (swattn_profile_supported)
+    if host and mode == MODE_SPARSE and _lib.lib().swattn_profile_supported(_lib.c_config(cfg)):
         O_h, lse_h = attend_host_chunked(Q, K, V, cfg, selection_mode)
         return _finish(O_h, lse_h, True), mode
     Qd, Kd, Vd = (to_device_bf16(x, nm) for x, nm in ((Q, "Q"), (K, "K"), (V, "V")))

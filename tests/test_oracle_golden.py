@@ -143,3 +143,24 @@ def test_dense_backward_matches_reference(name):
     _bf16_close(dQ, rec["dbwd_dQ_bits"])
     _bf16_close(dK, rec["dbwd_dK_bits"])
     _bf16_close(dV, rec["dbwd_dV_bits"])
+
+
+@pytest.mark.parametrize("name", ["paper_n8192_s0", "paper_n10000_s1"])
+def test_torch_f64_restatement_pinned(name):
+    """oracle/torch_f64.py (the full-size parity checker of the GPU tests)
+    reproduces the reference's own selection on every row of the goldens."""
+    import torch
+    from oracle import torch_f64
+    rec = load_golden(name)
+    c = [int(x) for x in rec["cfg"]]
+    prof = O.Profile(h_q=c[0], h_kv=c[1], d_h=c[2], B=c[3], l_C1=c[4], s_C1=c[5], l_C2=c[6],
+                     s_C2=c[7], l=c[8], s=c[9], N_init=c[10], N_local=c[11], k_top=c[12], w=c[13])
+    Q, K, V = O.draw_qkv(int(rec["n"]), prof.h_q, prof.h_kv, prof.d_h, int(rec["seed"]))
+
+    def t(x):
+        return torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16)
+    top = torch_f64.select_f64(t(Q), t(K), prof, rows_per_chunk=512).numpy()
+    assert np.array_equal(top, rec["topk"].astype(np.int64))
+    c1 = torch_f64.pool_bf16(t(K), prof.l_C1, prof.s_C1)
+    assert np.array_equal(c1.view(torch.int16).numpy().view(np.uint16),
+                          O.pool(K, prof.l_C1, prof.s_C1).view(np.uint16))
