@@ -97,6 +97,18 @@ static int num_sms() {
   return sms;
 }
 
+// Persistent CTAs of part B (one per SM by default).  SWATTN_PB_CTAS caps it
+// (measurement knob: part B is bound by the chip-wide L2 gather rate, so it
+// can leave SMs to concurrent work at little cost).
+static int part_b_ctas() {
+  static int ctas = [] {
+    const char *e = getenv("SWATTN_PB_CTAS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 && v < num_sms() ? v : num_sms();
+  }();
+  return ctas;
+}
+
 // The tensor-core kernels are the only path for the paper profile; the
 // CUDA-core kernels (scores_simt.cu / attention_simt.cu) serve the profiles
 // the tcgen05 tiles are not compiled for (e.g. the reference's small
@@ -513,9 +525,9 @@ static int32_t sparse_rows_impl(const swattn_config *cfg, const void *Q, const v
     if (!part_a_done && (rc = launch_sparse_part_a(cfg, Q, K, V, n, r0, r1, O, lse, m_a, l_a, st)))
       return rc;
     if ((rc = cuda_check(cudaMemsetAsync(slow_count, 0, 4, st), "memset(slow)"))) return rc;
-    if ((rc = launch_sparse_part_b(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, m_a, l_a, O, lse,
-                                   slow_count, slow_list, num_sms(), st)))
-      return rc;
+    rc = launch_sparse_part_b(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, m_a, l_a, O, lse,
+                              slow_count, slow_list, part_b_ctas(), st);
+    if (rc) return rc;
     return launch_attention_list(cfg, Q, K, V, n, topk, topk_cnt, slow_count, slow_list, O, lse,
                                  num_sms(), st);
   }

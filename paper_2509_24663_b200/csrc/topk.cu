@@ -25,6 +25,17 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kMaxCand = 4096;  // per-row candidate bound held in smem
 
+// A proven structural tie straddling the k-th boundary still needs the
+// float32 error-bound check against the nearest distinct keys on both sides
+// (the pair as a whole may belong above the next key up or below the next
+// key down in float64).
+__device__ __forceinline__ bool tie_neighbours_close(uint32_t T, uint32_t below, uint32_t above) {
+  const float vt = key2f(T);
+  const bool lo = below != 0u && (vt - key2f(below)) <= 3.0f * kScoreRelErr * fabsf(vt);
+  const bool hi = above != 0xffffffffu && (key2f(above) - vt) <= 3.0f * kScoreRelErr * fabsf(vt);
+  return lo || hi;
+}
+
 struct AmbList {
   int32_t *count;         // device counter
   int32_t *rows;          // [cap] row ids, then [cap] k-th keys (the re-rank's T)
@@ -116,16 +127,19 @@ __device__ void warp_topk_generic(const Keys ks, int ncand, int k, int N_init, i
   }
   const uint32_t T = prefix;
   int gt = 0, eq = 0;
-  uint32_t below = 0;  // largest key < T
+  uint32_t below = 0;             // largest key < T
+  uint32_t above = 0xffffffffu;   // smallest key > T
   for (int t = lane; t < ncand; t += 32) {
     const uint32_t v = ks[t];
     gt += v > T;
     eq += v == T;
     if (v < T && v > below) below = v;
+    if (v > T && v < above) above = v;
   }
   gt = __reduce_add_sync(0xffffffffu, gt);
   eq = __reduce_add_sync(0xffffffffu, eq);
   below = __reduce_max_sync(0xffffffffu, below);
+  above = __reduce_min_sync(0xffffffffu, above);
   const int need_eq = k - gt;
 
   // index-ordered compaction: key > T, or key == T among the first need_eq
@@ -170,7 +184,9 @@ __device__ void warp_topk_generic(const Keys ks, int ncand, int k, int N_init, i
         const int tj = j / 31, qj = j % 31, tj1 = (j + 1) / 31, qj1 = (j + 1) % 31;
         const bool R_j = (fr[tj] >> (2 * qj + 1)) & 1ull;
         const bool L_j1 = (fr[tj1] >> (2 * qj1)) & 1ull;
-        ambiguous = !(R_j && L_j1);
+        // the pair's own order is exact (equal float64 scores, lower index
+        // first); its order against the nearest other keys is not
+        ambiguous = !(R_j && L_j1) || tie_neighbours_close(T, below, above);
       }
     }
   } else {
@@ -373,10 +389,13 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
     }
   }
   uint32_t below = 0;  // largest key < T: a survivor unless T is the smallest one
+  uint32_t above = 0xffffffffu;  // smallest key > T (keys > T are all survivors)
   for (int t = lane; t < total; t += 32) {
     const uint32_t v = sc.key[t];
     if (v < T && v > below) below = v;
+    if (v > T && v < above) above = v;
   }
+  above = __reduce_min_sync(0xffffffffu, above);
   if (__reduce_max_sync(0xffffffffu, below) == 0u) {
 #pragma unroll 1
     for (int j = 0; j < kRegChunks; ++j) {
@@ -457,7 +476,9 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
         const int tj = j / 31, qj = j % 31, tj1 = (j + 1) / 31, qj1 = (j + 1) % 31;
         const bool R_j = (fr[tj] >> (2 * qj + 1)) & 1ull;
         const bool L_j1 = (fr[tj1] >> (2 * qj1)) & 1ull;
-        ambiguous = !(R_j && L_j1);
+        // the pair's own order is exact (equal float64 scores, lower index
+        // first); its order against the nearest other keys is not
+        ambiguous = !(R_j && L_j1) || tie_neighbours_close(T, below, above);
       }
     }
   } else {
