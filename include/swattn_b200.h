@@ -252,6 +252,8 @@ typedef struct swattn_paged_kv {
   void *kc2;
   int32_t max_m1;
   int32_t max_m2;
+  int32_t num_pages; /* pages in the k_pages / v_pages pools (bounds the TMA
+                        descriptors of the attention stage); 0 = batch * max_pages */
 } swattn_paged_kv;
 
 /* Recompute the compressed-key entries that became complete when the

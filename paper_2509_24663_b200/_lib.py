@@ -43,6 +43,7 @@ class CPagedKV(ctypes.Structure):
         ("kc2", ctypes.c_void_p),
         ("max_m1", ctypes.c_int32),
         ("max_m2", ctypes.c_int32),
+        ("num_pages", ctypes.c_int32),
     ]
 
 

@@ -23,11 +23,13 @@
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "tma_host.cuh"
 
 namespace swattn {
 
 int32_t launch_decode_topk(const swattn_config *, const float *, int64_t, const int32_t *, int, int,
-                           int32_t *, int32_t *, int32_t *, int32_t *, int32_t, cudaStream_t);
+                           int32_t *, int32_t *, int32_t *, int32_t *, int32_t, const uint64_t *,
+                           int64_t, cudaStream_t);
 int32_t launch_rerank_decode(const swattn_config *, const void *, const void *, const void *,
                              int max_m1, int max_m2, const int32_t *seq_lens, int batch,
                              const float *, int64_t, const int32_t *, const int32_t *, int32_t,
@@ -39,7 +41,8 @@ namespace {
 constexpr int kP1Cols = 128;     // normaliser columns per pass-1 CTA (4 warps x 32)
 constexpr int kTileBlocks = 31;  // pass-2 tile: 31 blocks, 124 (+4) columns
 constexpr int kTileCols = 128;
-constexpr int kAttnBlocks = 4;   // visible blocks per split-KV warp (24 splits at batch 16)
+constexpr int kP2Smem = 2 * kTileCols * 256 + 1024;  // passes 1 and 2: two 128-row key tiles
+constexpr int kAttnBlocks = 3;   // visible blocks per split-KV warp (32 splits: 1024 warps at batch 16 = one wave)
 
 struct DecodeArgs {
   const __nv_bfloat16 *q;            // [batch][h_q][d]
@@ -103,7 +106,31 @@ __device__ __forceinline__ void mma16816_p1(float (&c)[4], const uint32_t (&a)[4
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// Persistent over 128-column slices like pass 2: grid (rows, kP1Ctas), CTA y
+// takes slices y, y + kP1Ctas, ..., the next slice's key rows in flight
+// (cp.async, double buffer) while the current one is scored from shared
+// memory (ldmatrix); one (max, sum) partial per slice and head, merged in
+// the same order as before (n-tiles of a lane, the lane quad, the 4 warps).
+constexpr int kP1Ctas = 8;
+
+__device__ __forceinline__ void p1_issue_slice(uint32_t kt, const __nv_bfloat16 *kbase, int64_t col0,
+                                               int64_t vis, int h_kv) {
+  for (int c = threadIdx.x; c < kP1Cols * 16; c += blockDim.x) {
+    const int rr = c >> 4, ch = c & 15;
+    const uint32_t dst = kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4);
+    const int64_t col = col0 + rr;
+    if (col < vis)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(kbase + col * h_kv * kD + ch * 8));
+    else
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0u));
+  }
+  asm volatile("cp.async.commit_group;");
+}
+
 __global__ void __launch_bounds__(128) decode_pass1_kernel(DecodeArgs a, float2 *part, int splits) {
+  extern __shared__ uint8_t p1_raw[];
+  uint8_t *ktiles = p1_raw + ((128u - (tc::smem_u32(p1_raw) & 127u)) & 127u);  // [2][128 rows][256 B]
   __shared__ float2 red[4][kG];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
@@ -111,15 +138,17 @@ __global__ void __launch_bounds__(128) decode_pass1_kernel(DecodeArgs a, float2 
   const int64_t vis1 = vis_count(L - 1, a.l_C1, a.s_C1);
   const bool use2 = vis2 > 0;
   const int64_t vis = use2 ? vis2 : vis1;  // fallback rows use the exact C1 lse
+  const int n_sl = (int)min((int64_t)splits, cdiv(vis, (int64_t)kP1Cols));
+  if ((int)blockIdx.y >= n_sl) return;
   const __nv_bfloat16 *kc = (use2 ? a.kc2 : a.kc1) + ((int64_t)seq * (use2 ? a.max_m2 : a.max_m1) * a.h_kv + g) * kD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, dw = lane & 3;
-  const int64_t col0 = (int64_t)blockIdx.y * 128 + warp * 32;
-  float m0 = -INFINITY, l0 = 0.f, m1 = -INFINITY, l1 = 0.f;  // heads r, r + 8
-  if (col0 < vis) {
+  const uint32_t kt0 = tc::smem_u32(ktiles);
+  p1_issue_slice(kt0, kc, (int64_t)blockIdx.y * kP1Cols, vis, a.h_kv);
+  uint32_t qa[8][4];
+  {
     const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.q + (((int64_t)seq * a.h_q + g * kG + r) * kD));
     const uint32_t *q1 = q0 + 8 * (kD / 2);
-    uint32_t qa[8][4];
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       qa[ks][0] = __ldg(q0 + ks * 8 + dw);
@@ -127,48 +156,67 @@ __global__ void __launch_bounds__(128) decode_pass1_kernel(DecodeArgs a, float2 
       qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
       qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
     }
+  }
+  const int lm = lane >> 3, lr = lane & 7;
+  int buf = 0;
+  for (int sl = blockIdx.y; sl < n_sl; sl += gridDim.y, buf ^= 1) {
+    const uint32_t kt = kt0 + buf * (kP1Cols * 256);
+    if (sl + (int)gridDim.y < n_sl) {
+      p1_issue_slice(kt0 + (buf ^ 1) * (kP1Cols * 256), kc, (int64_t)(sl + gridDim.y) * kP1Cols, vis, a.h_kv);
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
+    }
+    __syncthreads();
+    const int64_t col0 = (int64_t)sl * kP1Cols + warp * 32;
+    float acc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int rr = warp * 32 + hf * 16 + (lm >> 1) * 8 + lr, ch = ks * 2 + (lm & 1);
+        uint32_t b00, b01, b10, b11;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b00), "=r"(b01), "=r"(b10), "=r"(b11)
+                     : "r"(kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4)));
+        mma16816_p1(acc[2 * hf], qa[ks], b00, b01);
+        mma16816_p1(acc[2 * hf + 1], qa[ks], b10, b11);
+      }
+    }
+    float m0 = -INFINITY, l0 = 0.f, m1 = -INFINITY, l1 = 0.f;  // heads r, r + 8
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      const int64_t col = col0 + nt * 8 + r;
-      const bool ok = col < vis;
-      const uint32_t *kr = reinterpret_cast<const uint32_t *>(kc + (ok ? col : 0) * a.h_kv * kD);
-      uint32_t kb[8][2];
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        kb[ks][0] = ok ? __ldg(kr + ks * 8 + dw) : 0u;
-        kb[ks][1] = ok ? __ldg(kr + ks * 8 + 4 + dw) : 0u;
-      }
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) mma16816_p1(acc, qa[ks], kb[ks][0], kb[ks][1]);
       // columns 2 dw, 2 dw + 1 of this n-tile
       const int64_t c = col0 + nt * 8 + 2 * dw;
       const bool v0 = c < vis, v1 = c + 1 < vis;
-      const float x0 = v0 ? acc[0] * a.scale_log2 : -INFINITY, x1 = v1 ? acc[1] * a.scale_log2 : -INFINITY;
-      const float x2 = v0 ? acc[2] * a.scale_log2 : -INFINITY, x3 = v1 ? acc[3] * a.scale_log2 : -INFINITY;
+      const float x0 = v0 ? acc[nt][0] * a.scale_log2 : -INFINITY, x1 = v1 ? acc[nt][1] * a.scale_log2 : -INFINITY;
+      const float x2 = v0 ? acc[nt][2] * a.scale_log2 : -INFINITY, x3 = v1 ? acc[nt][3] * a.scale_log2 : -INFINITY;
       const float mm0 = fmaxf(x0, x1), mm1 = fmaxf(x2, x3);
       if (mm0 != -INFINITY) merge_ml(m0, l0, mm0, fast_exp2(x0 - mm0) + fast_exp2(x1 - mm0));
       if (mm1 != -INFINITY) merge_ml(m1, l1, mm1, fast_exp2(x2 - mm1) + fast_exp2(x3 - mm1));
     }
-  }
-  // lanes 4 r .. 4 r + 3 share head rows r and r + 8
+    // lanes 4 r .. 4 r + 3 share head rows r and r + 8
 #pragma unroll
-  for (int o = 1; o < 4; o <<= 1) {
-    const float om0 = __shfl_xor_sync(0xffffffffu, m0, o), ol0 = __shfl_xor_sync(0xffffffffu, l0, o);
-    const float om1 = __shfl_xor_sync(0xffffffffu, m1, o), ol1 = __shfl_xor_sync(0xffffffffu, l1, o);
-    merge_ml(m0, l0, om0, ol0);
-    merge_ml(m1, l1, om1, ol1);
-  }
-  if (dw == 0) {
-    red[warp][r] = make_float2(m0, l0);
-    red[warp][r + 8] = make_float2(m1, l1);
-  }
-  __syncthreads();
-  if (threadIdx.x < kG) {
-    const int h = threadIdx.x;
-    float M = -INFINITY, S = 0.f;
-    for (int w = 0; w < 4; ++w) merge_ml(M, S, red[w][h].x, red[w][h].y);
-    part[((int64_t)row * splits + blockIdx.y) * kG + h] = make_float2(M, S);
+    for (int o = 1; o < 4; o <<= 1) {
+      const float om0 = __shfl_xor_sync(0xffffffffu, m0, o), ol0 = __shfl_xor_sync(0xffffffffu, l0, o);
+      const float om1 = __shfl_xor_sync(0xffffffffu, m1, o), ol1 = __shfl_xor_sync(0xffffffffu, l1, o);
+      merge_ml(m0, l0, om0, ol0);
+      merge_ml(m1, l1, om1, ol1);
+    }
+    if (dw == 0) {
+      red[warp][r] = make_float2(m0, l0);
+      red[warp][r + 8] = make_float2(m1, l1);
+    }
+    __syncthreads();  // red complete; every warp is done with tile buffer `buf`
+    if (threadIdx.x < kG) {
+      const int h = threadIdx.x;
+      float M = -INFINITY, S = 0.f;
+      for (int w = 0; w < 4; ++w) merge_ml(M, S, red[w][h].x, red[w][h].y);
+      part[((int64_t)row * splits + sl) * kG + h] = make_float2(M, S);
+    }
+    __syncthreads();  // red reuse
   }
 }
 
@@ -188,9 +236,45 @@ __device__ __forceinline__ void mma16816_dec(float (&c)[4], const uint32_t (&a)[
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ unsigned long long spread_bits2(uint32_t x) {  // bit q -> bit 2q
+  unsigned long long v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// Persistent over tiles: grid (rows, kP2Ctas); CTA y handles tiles y,
+// y + kP2Ctas, ... of its row with the next tile's 32 KB of C1 rows in flight
+// (cp.async, double buffer) while the current one is scored, and merges the
+// row's pass-1 partials and loads q once (a CTA per tile repeated both 67
+// times per row and ran 2.4 short waves: 26-31 us, profiles/r02k).
+constexpr int kP2Ctas = 8;
+
+__device__ __forceinline__ void p2_issue_tile(uint32_t kt, const __nv_bfloat16 *kbase, int64_t tile0,
+                                              int64_t vis1, int h_kv) {
+  // 128 C1 rows -> shared memory (256-byte rows, 16-byte chunk c of row rr at
+  // c ^ (rr & 7): conflict-free ldmatrix), zeros past vis1
+  for (int c = threadIdx.x; c < kTileCols * 16; c += blockDim.x) {
+    const int rr = c >> 4, ch = c & 15;
+    const uint32_t dst = kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4);
+    const int64_t col = tile0 + rr;
+    if (col < vis1)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(kbase + col * h_kv * kD + ch * 8));
+    else
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0u));
+  }
+  asm volatile("cp.async.commit_group;");
+}
+
 __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const float2 *part,
-                                                           int splits, float *s_cmp, int64_t ld) {
-  __shared__ __align__(128) uint8_t ktile[kTileCols * 256];  // 32 KB of C1 rows
+                                                           int splits, float *s_cmp, int64_t ld,
+                                                           uint64_t *flags, int ld_f) {
+  extern __shared__ uint8_t p2_raw[];
+  uint8_t *ktiles = p2_raw + ((128u - (tc::smem_u32(p2_raw) & 127u)) & 127u);  // [2][128 rows][256 B]
   __shared__ float2 stat[kG];  // (m, 1/l), log2 domain
   __shared__ float sc[kTileCols + 4];
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
@@ -199,24 +283,36 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
   const int64_t m1 = num_pooled(L, a.l_C1, a.s_C1);
   const int n_cols = (int)(m1 ? cdiv(m1, kPoolS) : 0);
   const int hi = cand_hi((int)(i / a.B), a.N_local, n_cols);
-  const int t = blockIdx.y;
-  if (t * kTileBlocks >= hi) return;
+  const int n_tiles = (int)cdiv(hi, kTileBlocks);
+  if ((int)blockIdx.y >= n_tiles) return;
   const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const __nv_bfloat16 *kbase = a.kc1 + ((int64_t)seq * a.max_m1 * a.h_kv + g) * kD;
+  const uint32_t kt0 = tc::smem_u32(ktiles);
+  p2_issue_tile(kt0, kbase, (int64_t)blockIdx.y * kTileBlocks * kPoolS, vis1, a.h_kv);
   if (warp == 0) {
     // pass-1 partials of this row: only the slices pass 1 covered hold data
     // (C2 columns for approx rows, C1 for fallback rows); lane pairs (h, half)
-    // merge half of the slices each, then one shuffle joins the halves
+    // merge half of the slices each (eight independent loads per round), then
+    // one shuffle joins the halves
     const int64_t vis2 = vis_count(i, a.l_C2, a.s_C2);
     const int used = (int)min((int64_t)splits, cdiv(vis2 > 0 ? vis2 : vis1, (int64_t)kP1Cols));
     const int h = lane & 15, half = lane >> 4;
     float M = -INFINITY, S = 0.f;
-    for (int sp = half; sp < used; sp += 2) {
-      const float2 pv = part[((int64_t)row * splits + sp) * kG + h];
-      if (pv.x == -INFINITY) continue;
-      const float Mn = fmaxf(M, pv.x);
-      S = (M == -INFINITY ? 0.f : S * fast_exp2(M - Mn)) + pv.y * fast_exp2(pv.x - Mn);
-      M = Mn;
+    for (int sp0 = 0; sp0 < used; sp0 += 16) {
+      float2 pv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int sp = sp0 + 2 * e + half;
+        pv[e] = sp < used ? part[((int64_t)row * splits + sp) * kG + h] : make_float2(-INFINITY, 0.f);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (pv[e].x == -INFINITY) continue;
+        const float Mn = fmaxf(M, pv[e].x);
+        S = (M == -INFINITY ? 0.f : S * fast_exp2(M - Mn)) + pv[e].y * fast_exp2(pv[e].x - Mn);
+        M = Mn;
+      }
     }
     const float oM = __shfl_xor_sync(0xffffffffu, M, 16), oS = __shfl_xor_sync(0xffffffffu, S, 16);
     const float Mt = fmaxf(M, oM);
@@ -237,73 +333,78 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
     qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
     qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
   }
-  // the tile's 128 C1 rows -> shared memory by cp.async (256-byte rows, 16-byte
-  // chunk c of row rr at c ^ (rr & 7): conflict-free ldmatrix), zeros past vis1
-  const int64_t tile0 = (int64_t)t * kTileBlocks * kPoolS;
-  const __nv_bfloat16 *kbase = a.kc1 + ((int64_t)seq * a.max_m1 * a.h_kv + g) * kD;
-  const uint32_t kt = tc::smem_u32(ktile);
-  for (int c = threadIdx.x; c < kTileCols * 16; c += blockDim.x) {
-    const int rr = c >> 4, ch = c & 15;
-    const uint32_t dst = kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4);
-    const int64_t col = tile0 + rr;
-    if (col < vis1)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                   "l"(kbase + col * a.h_kv * kD + ch * 8));
-    else
-      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0u));
-  }
-  asm volatile("cp.async.commit_group;");
-  asm volatile("cp.async.wait_group 0;");
-  const int64_t col0 = tile0 + warp * 32;
-  float acc[4][4];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-  __syncthreads();  // tile and stat
   const int lm = lane >> 3, lr = lane & 7;
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      // rows (columns) 32 warp + 16 hf + 8 (lm >> 1) + lr; matrices (n-tile lo, k lo),
-      // (n-tile lo, k hi), (n-tile hi, k lo), (n-tile hi, k hi)
-      const int rr = warp * 32 + hf * 16 + (lm >> 1) * 8 + lr, ch = ks * 2 + (lm & 1);
-      uint32_t b00, b01, b10, b11;
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(b00), "=r"(b01), "=r"(b10), "=r"(b11)
-                   : "r"(kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4)));
-      mma16816_dec(acc[2 * hf], qa[ks], b00, b01);
-      mma16816_dec(acc[2 * hf + 1], qa[ks], b10, b11);
+  int buf = 0;
+  for (int t = blockIdx.y; t < n_tiles; t += gridDim.y, buf ^= 1) {
+    const int64_t tile0 = (int64_t)t * kTileBlocks * kPoolS;
+    const uint32_t kt = kt0 + buf * (kTileCols * 256);
+    if (t + (int)gridDim.y < n_tiles) {
+      p2_issue_tile(kt0 + (buf ^ 1) * (kTileCols * 256), kbase,
+                    (int64_t)(t + gridDim.y) * kTileBlocks * kPoolS, vis1, a.h_kv);
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
     }
-  }
-  const float2 st0 = stat[r], st1 = stat[r + 8];
+    __syncthreads();  // tile t (all threads' copies) and stat
+    const int64_t col0 = tile0 + warp * 32;
+    float acc[4][4];
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    // rows r (c0, c1) and r + 8 (c2, c3); columns 2 (lane % 4) + {0, 1}
-    float c0 = fast_exp2(fmaf(acc[nt][0], a.scale_log2, -st0.x)) * st0.y +
-               fast_exp2(fmaf(acc[nt][2], a.scale_log2, -st1.x)) * st1.y;
-    float c1 = fast_exp2(fmaf(acc[nt][1], a.scale_log2, -st0.x)) * st0.y +
-               fast_exp2(fmaf(acc[nt][3], a.scale_log2, -st1.x)) * st1.y;
+    for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-    }
-    if (r == 0) {
-      const int cc = warp * 32 + nt * 8 + 2 * dw;
-      const int64_t col = col0 + nt * 8 + 2 * dw;
-      sc[cc] = col < m1 ? (col < vis1 ? c0 : 0.f) : -INFINITY;
-      sc[cc + 1] = col + 1 < m1 ? (col + 1 < vis1 ? c1 : 0.f) : -INFINITY;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < kTileBlocks) {
-    const int j = t * kTileBlocks + threadIdx.x;
-    if (j >= a.N_init && j < hi) {
-      float mx = sc[threadIdx.x * kPoolS];
+    for (int ks = 0; ks < 8; ++ks) {
 #pragma unroll
-      for (int e = 1; e < kPoolL; ++e) mx = fmaxf(mx, sc[threadIdx.x * kPoolS + e]);
-      s_cmp[(int64_t)row * ld + j] = mx;
+      for (int hf = 0; hf < 2; ++hf) {
+        // rows (columns) 32 warp + 16 hf + 8 (lm >> 1) + lr; matrices (n-tile lo, k lo),
+        // (n-tile lo, k hi), (n-tile hi, k lo), (n-tile hi, k hi)
+        const int rr = warp * 32 + hf * 16 + (lm >> 1) * 8 + lr, ch = ks * 2 + (lm & 1);
+        uint32_t b00, b01, b10, b11;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b00), "=r"(b01), "=r"(b10), "=r"(b11)
+                     : "r"(kt + rr * 256 + (uint32_t)(((ch & 8) | ((ch & 7) ^ (rr & 7))) << 4)));
+        mma16816_dec(acc[2 * hf], qa[ks], b00, b01);
+        mma16816_dec(acc[2 * hf + 1], qa[ks], b10, b11);
+      }
     }
+    const float2 st0 = stat[r], st1 = stat[r + 8];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      // rows r (c0, c1) and r + 8 (c2, c3); columns 2 (lane % 4) + {0, 1}
+      float c0 = fast_exp2(fmaf(acc[nt][0], a.scale_log2, -st0.x)) * st0.y +
+                 fast_exp2(fmaf(acc[nt][2], a.scale_log2, -st1.x)) * st1.y;
+      float c1 = fast_exp2(fmaf(acc[nt][1], a.scale_log2, -st0.x)) * st0.y +
+                 fast_exp2(fmaf(acc[nt][3], a.scale_log2, -st1.x)) * st1.y;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      }
+      if (r == 0) {
+        const int cc = warp * 32 + nt * 8 + 2 * dw;
+        const int64_t col = col0 + nt * 8 + 2 * dw;
+        sc[cc] = col < m1 ? (col < vis1 ? c0 : 0.f) : -INFINITY;
+        sc[cc + 1] = col + 1 < m1 ? (col + 1 < vis1 ? c1 : 0.f) : -INFINITY;
+      }
+    }
+    __syncthreads();  // sc complete; every warp is done reading tile buffer `buf`
+    if (warp == 0) {
+      // 5/4 max-pool, one block per lane, plus the argmax-at-shared-column bits
+      // (L: window column 0, R: column 4, with margin) that let top-k settle a
+      // structural tie straddling the k-th boundary without the float64
+      // re-rank -- the same flags K2 emits for prefill (scores_tc.cu)
+      const int j = t * kTileBlocks + lane;
+      const bool ok = lane < kTileBlocks && j >= a.N_init && j < hi;
+      float v[kPoolL];
+#pragma unroll
+      for (int e = 0; e < kPoolL; ++e) v[e] = sc[min(lane * kPoolS + e, kTileCols + 3)];
+      if (ok) s_cmp[(int64_t)row * ld + j] = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), v[4]);
+      const float f = 1.f + 4.f * kScoreRelErr;
+      const bool Lb = ok && v[1] * f < v[0] && v[2] * f < v[0] && v[3] * f < v[0] && v[4] * f < v[0];
+      const bool Rb = ok && v[0] * f < v[4] && v[1] * f < v[4] && v[2] * f < v[4] && v[3] * f < v[4];
+      const unsigned lmask = __ballot_sync(0xffffffffu, Lb);
+      const unsigned rmask = __ballot_sync(0xffffffffu, Rb);
+      if (lane == 0) flags[(int64_t)row * ld_f + t] = spread_bits2(lmask) | (spread_bits2(rmask) << 1);
+    }
+    __syncthreads();  // sc reuse by the next tile
   }
 }
 
@@ -319,11 +420,15 @@ __device__ __forceinline__ int visible_block(int idx, int n_init, int ntop, cons
 // ---- D5 on the tensor cores: one warp = (row, split of kAttnBlocks blocks);
 // the row's 16 query heads are the M = 16 of mma.sync.m16n8k16 (as in the
 // prefill part B, csrc/sparse_warp.cu): Q in registers, S -> P in registers,
-// O in registers, online softmax per 16-key stage.  K/V rows are gathered
-// from the page pool with cp.async into a per-warp 2-stage ring stored
-// [d half][row][64] with the 16-byte chunk XOR-swizzled by row, so the
-// ldmatrix reads are conflict-free.
-constexpr int kDW = 4;                        // warps per CTA
+// O in registers, online softmax per 16-key stage.  K/V stages (16 rows of
+// one page) come from the page pool by TMA -- one 4-D box {64 d, 16 rows,
+// 2 d-halves, 1 group} per tensor into a per-warp 3-slot mbarrier ring
+// stored [d half][row][64] with the 128-byte swizzle (conflict-free
+// ldmatrix), lane 0 the warp's issuer -- the part-B scheme of
+// csrc/sparse_warp.cu.  (16-byte cp.async copies needed ~60 instructions per
+// stage per lane and reached 3.6 TB/s, profiles/r02o.)
+constexpr int kDW = 2;                        // warps per CTA (4 CTAs, 8 warps per SM)
+constexpr int kDStages = 3;                   // ring depth: 2 stages in flight while one computes
 constexpr int kDStageKeys = 16;
 constexpr uint32_t kDTile = kDStageKeys * kD * 2;  // 4 KB
 
@@ -352,17 +457,28 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t *>(&v);
 }
 
+struct AttnMaps {
+  CUtensorMap k, v;  // page pools as (d lo/hi 64, pool row, half, group): box {64, 16, 2, 1}
+};
+
 __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a, const int32_t *topk,
                                                                   const int32_t *topk_cnt,
                                                                   float *part_o, float2 *part_ml,
-                                                                  int splits) {
+                                                                  int splits,
+                                                                  const __grid_constant__ AttnMaps maps) {
   extern __shared__ uint8_t dsm_raw[];
   uint8_t *dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
-  auto ring = reinterpret_cast<uint8_t(*)[2][2][kDTile]>(dsm);  // [warp][stage][K|V]
-  auto qs = reinterpret_cast<__nv_bfloat16(*)[kG * kD]>(dsm + kDW * 4 * kDTile);
+  auto ring = reinterpret_cast<uint8_t(*)[kDStages][2][kDTile]>(dsm);  // [warp][stage][K|V]
+  __shared__ uint64_t full_s[kDW][kDStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * kDW + warp;
   if (unit >= a.batch * a.h_kv * splits) return;
+  uint64_t *full = full_s[warp];
+  if (lane == 0) {
+    for (int k = 0; k < kDStages; ++k) tc::mbar_init(&full[k], 1);
+    tc::fence_barrier_init();
+  }
+  __syncwarp();
   const int row = unit / splits, split = unit % splits;
   const int seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
@@ -385,49 +501,55 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
     }
     return;
   }
-  // q rows of the group -> smem (row-major, 256 B) -> A fragments
-  const __nv_bfloat16 *qg = a.q + ((int64_t)seq * a.h_q + g * kG) * kD;
-  for (int e = lane; e < kG * kD / 8; e += 32)
-    reinterpret_cast<uint4 *>(qs[warp])[e] = reinterpret_cast<const uint4 *>(qg)[e];
-  __syncwarp();
+  // q of the group as A fragments straight from global memory:
+  // a0 = (head h0, d k), a1 = (h0 + 8, k), a2 = (h0, k + 8), a3 = (h0 + 8, k + 8)
   const int lm = lane >> 3, lr = lane & 7;
   uint32_t qa[8][4];
+  {
+    const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.q + (((int64_t)seq * a.h_q + g * kG + h0) * kD));
+    const uint32_t *q1 = q0 + 8 * (kD / 2);
+    const int dw = lane & 3;
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-    // matrices: (heads 0-7, d lo), (heads 8-15, d lo), (heads 0-7, d hi), (heads 8-15, d hi)
-    const int head = (lm & 1) * 8 + lr, d = ks * 16 + (lm >> 1) * 8;
-    const uint32_t addr = tc::smem_u32(&qs[warp][head * kD + d]);
-    dldsm_x4(addr, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], false);
+    for (int ks = 0; ks < 8; ++ks) {
+      qa[ks][0] = __ldg(q0 + ks * 8 + dw);
+      qa[ks][1] = __ldg(q1 + ks * 8 + dw);
+      qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
+      qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
+    }
+  }
+  // the warp's <= kAttnBlocks block ids and their pages, looked up once
+  // (lane l holds block vb0 + l): a per-stage topk -> block_table -> page
+  // chain of dependent loads was the kernel's top stall (profiles/r02n)
+  int my_j = 0, my_page = 0;
+  if (lane < vb1 - vb0) {
+    my_j = visible_block(vb0 + lane, n_init, ntop, top, lo2);
+    my_page = a.block_table[(int64_t)seq * a.max_pages + my_j];
   }
   // stage s of this warp's key stream: block vb0 + s / 4, rows (s % 4) * 16 ..
   const int nst = (vb1 - vb0) * (kB / kDStageKeys);
-  auto issue = [&](int st_idx, int slot) {
-    const int j = visible_block(vb0 + st_idx / 4, n_init, ntop, top, lo2);
-    const int page = a.block_table[(int64_t)seq * a.max_pages + j];
-    const int r0 = (st_idx % 4) * kDStageKeys;
-    // 16 rows x 16 chunks of 16 B per tensor: 8 per lane
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int idx = e * 32 + lane, rr = idx >> 4, c = idx & 15;
-      const int64_t off = (((int64_t)page * kB + r0 + rr) * a.h_kv + g) * kD + c * 8;
-      const uint32_t dk = tc::smem_u32(ring[warp][slot][0]) + dswz(rr, c);
-      const uint32_t dv = tc::smem_u32(ring[warp][slot][1]) + dswz(rr, c);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dk), "l"(a.k_pages + off));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dv), "l"(a.v_pages + off));
+  auto issue = [&](int st_idx, int slot) {  // warp-collective (the shuffle); lane 0 issues
+    const int page = __shfl_sync(0xffffffffu, my_page, st_idx / 4);
+    if (lane == 0) {
+      const int prow = page * kB + (st_idx % 4) * kDStageKeys;
+      tc::mbar_arrive_expect_tx(&full[slot], 2 * kDTile);
+      tc::tma_load_4d(&maps.k, &full[slot], ring[warp][slot][0], 0, prow, 0, g);
+      tc::tma_load_4d(&maps.v, &full[slot], ring[warp][slot][1], 0, prow, 0, g);
     }
-    asm volatile("cp.async.commit_group;");
   };
-  issue(0, 0);
-  if (nst > 1) issue(1, 1);
+  for (int s0 = 0; s0 < kDStages && s0 < nst; ++s0) issue(s0, s0);
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   float o[16][4];
 #pragma unroll
   for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   for (int s2 = 0; s2 < nst; ++s2) {
-    const int slot = s2 & 1;
-    if (s2 + 1 < nst) asm volatile("cp.async.wait_group 1;");
-    else asm volatile("cp.async.wait_group 0;");
-    __syncwarp();
+    const int slot = s2 % kDStages;
+    // refill the slot stage s2 - 1 used (every lane finished reading it at
+    // the end of the previous iteration) with stage s2 + kDStages - 1
+    if (s2 >= 1 && s2 + kDStages - 1 < nst) {
+      if (lane == 0) tc::fence_proxy_async();
+      issue(s2 + kDStages - 1, (s2 + kDStages - 1) % kDStages);
+    }
+    tc::mbar_wait(&full[slot], (uint32_t)((s2 / kDStages) & 1));
     const uint32_t kst = tc::smem_u32(ring[warp][slot][0]), vst = tc::smem_u32(ring[warp][slot][1]);
     float sc[2][4] = {};
 #pragma unroll
@@ -438,7 +560,7 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
       dmma(sc[1], qa[ks], b10, b11);
     }
     // causal clip: keys after i (only in the diagonal block) are masked
-    const int j = visible_block(vb0 + s2 / 4, n_init, ntop, top, lo2);
+    const int j = __shfl_sync(0xffffffffu, my_j, s2 / 4);
     const int64_t key0 = (int64_t)j * kB + (s2 % 4) * kDStageKeys;
     float x[2][4];
     float mx0 = -INFINITY, mx1 = -INFINITY;
@@ -488,8 +610,7 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
       dmma(o[2 * dp], pa, v00, v01);
       dmma(o[2 * dp + 1], pa, v10, v11);
     }
-    __syncwarp();
-    if (s2 + 2 < nst) issue(s2 + 2, slot);
+    __syncwarp();  // every lane's reads of this slot are done before it is refilled
   }
   // partial row sums over the quad, then the partial state of this split
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
@@ -508,13 +629,13 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
   }
 }
 
-// grid (batch*h_kv), 512 threads = 16 heads x 32 lanes (4 d each)
-__global__ void __launch_bounds__(512) decode_combine_kernel(DecodeArgs a, const int32_t *topk_cnt,
+// grid (batch*h_kv, 4), 128 threads = 4 heads x 32 lanes (4 d each)
+__global__ void __launch_bounds__(128) decode_combine_kernel(DecodeArgs a, const int32_t *topk_cnt,
                                                              const float *part_o,
                                                              const float2 *part_ml, int splits,
                                                              __nv_bfloat16 *o, float *lse) {
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int64_t L = a.seq_lens[seq];
   if (L < 1) {  // empty slot: defined outputs (O = 0, lse = -inf), nothing read
     o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 0] = __float2bfloat16_rn(0.f);
@@ -528,22 +649,24 @@ __global__ void __launch_bounds__(512) decode_combine_kernel(DecodeArgs a, const
   const int n_init = min(a.N_init, b + 1);
   const int lo2 = max(max(0, b - a.N_local + 1), n_init);
   const int nvis = n_init + topk_cnt[row] + (b + 1 - lo2);
-  const int used = (int)cdiv(nvis, kAttnBlocks);  // <= 24 splits (96 blocks / 4)
-  // lane s holds split s's (max, sum): one load, then warp reductions
-  float2 ml = make_float2(-INFINITY, 0.f);
-  if (lane < used) ml = part_ml[((int64_t)row * splits + lane) * kG + h];
-  float M = ml.x;
+  const int used = (int)cdiv(nvis, kAttnBlocks);  // <= 64 splits ((64 + kTopMax) blocks / 3)
+  // lane s holds splits s and s + 32 (<= 64 splits): two loads, warp reductions
+  float2 ml0 = make_float2(-INFINITY, 0.f), ml1 = make_float2(-INFINITY, 0.f);
+  if (lane < used) ml0 = part_ml[((int64_t)row * splits + lane) * kG + h];
+  if (lane + 32 < used) ml1 = part_ml[((int64_t)row * splits + lane + 32) * kG + h];
+  float M = fmaxf(ml0.x, ml1.x);
 #pragma unroll
   for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  const float wl = ml.x == -INFINITY ? 0.f : fast_exp2(ml.x - M);
-  float Ls = ml.y * wl;
+  const float wl0 = ml0.x == -INFINITY ? 0.f : fast_exp2(ml0.x - M);
+  const float wl1 = ml1.x == -INFINITY ? 0.f : fast_exp2(ml1.x - M);
+  float Ls = ml0.y * wl0 + ml1.y * wl1;
 #pragma unroll
   for (int off = 16; off; off >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, off);
-  // the splits' partial O rows are independent loads (4 in flight)
+  // the splits' partial O rows are independent loads (8 in flight)
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
+#pragma unroll 8
   for (int sp = 0; sp < used; ++sp) {
-    const float w = __shfl_sync(0xffffffffu, wl, sp);
+    const float w = __shfl_sync(0xffffffffu, sp < 32 ? wl0 : wl1, sp & 31);
     const int64_t pi = ((int64_t)row * splits + sp) * kG + h;
     const float4 po = *reinterpret_cast<const float4 *>(&part_o[pi * kD + 4 * lane]);
     if (w != 0.f) {
@@ -593,7 +716,7 @@ static DecodeArgs make_args(const swattn_config *cfg, const swattn_paged_kv *kv,
 struct DecodeLayout {
   int p1_splits, tiles, attn_splits, max_ctx;
   int64_t ld;
-  size_t off_p1, off_scmp, off_topk, off_cnt, off_count, off_rows, off_part, off_po, off_pml, total;
+  size_t off_p1, off_scmp, off_flags, off_topk, off_cnt, off_count, off_rows, off_part, off_po, off_pml, total;
 };
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -604,6 +727,7 @@ static DecodeLayout decode_layout(const swattn_config *cfg, int batch, int max_p
   const int64_t m1 = num_pooled(D.max_ctx, cfg->l_C1, cfg->s_C1);
   const int64_t m2 = num_pooled(D.max_ctx, cfg->l_C2, cfg->s_C2);
   const int64_t n_cols = m1 ? cdiv(m1, cfg->s) : 0;
+  static_assert(64 + kTopMax <= 64 * kAttnBlocks, "decode_combine_kernel keeps two splits per lane");
   D.p1_splits = (int)std::max<int64_t>(1, cdiv(std::max(m2, m1), kP1Cols));
   D.tiles = (int)std::max<int64_t>(1, cdiv(n_cols, kTileBlocks));
   D.attn_splits = (int)cdiv(cfg->N_init + cfg->N_local + cfg->k_top, kAttnBlocks);
@@ -612,6 +736,7 @@ static DecodeLayout decode_layout(const swattn_config *cfg, int batch, int max_p
   size_t o = 0;
   D.off_p1 = o; o = al(o + rows * D.p1_splits * kG * sizeof(float2));
   D.off_scmp = o; o = al(o + rows * D.ld * sizeof(float));
+  D.off_flags = o; o = al(o + rows * D.tiles * sizeof(uint64_t));
   D.off_topk = o; o = al(o + rows * std::max(cfg->k_top, 1) * sizeof(int32_t));
   D.off_cnt = o; o = al(o + rows * sizeof(int32_t));
   D.off_count = o; o = al(o + 16);
@@ -704,13 +829,29 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
   float2 *pml = reinterpret_cast<float2 *>(ws + D.off_pml);
   DecodeArgs a = make_args(cfg, kv, q, batch);
   const int nrows = batch * cfg->h_kv;
-  decode_pass1_kernel<<<dim3(nrows, D.p1_splits), 128, 0, st>>>(a, p1, D.p1_splits);
+  {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(decode_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2Smem);
+      attr = true;
+    }
+    decode_pass1_kernel<<<dim3(nrows, kP1Ctas), 128, kP2Smem, st>>>(a, p1, D.p1_splits);
+  }
   SWATTN_LAUNCH_CHECK("decode_pass1_kernel");
-  decode_pass2_kernel<<<dim3(nrows, D.tiles), 128, 0, st>>>(a, p1, D.p1_splits, scmp, D.ld);
+  uint64_t *flags = reinterpret_cast<uint64_t *>(ws + D.off_flags);
+  {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(decode_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2Smem);
+      attr = true;
+    }
+    decode_pass2_kernel<<<dim3(nrows, kP2Ctas), 128, kP2Smem, st>>>(a, p1, D.p1_splits, scmp, D.ld,
+                                                                   flags, D.tiles);
+  }
   SWATTN_LAUNCH_CHECK("decode_pass2_kernel");
   if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset"))) return rc;
   if ((rc = launch_decode_topk(cfg, scmp, D.ld, kv->seq_lens, batch, D.max_ctx, topk, cnt, count,
-                               rows, nrows, st)))
+                               rows, nrows, flags, D.tiles, st)))
     return rc;
   if ((rc = launch_rerank_decode(cfg, q, kv->kc1, kv->kc2, kv->max_m1, kv->max_m2, kv->seq_lens,
                                  batch, scmp, D.ld, count, rows, nrows, topk, ws + D.off_part,
@@ -718,17 +859,30 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
     return rc;
   {
     const int units = nrows * D.attn_splits;
-    const int smem = kDW * 4 * kDTile + kDW * kG * kD * 2 + 1024;
+    const int smem = kDW * kDStages * 2 * kDTile + 1024;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
+    AttnMaps maps;
+    {
+      // the pools as (d lo/hi 64, pool row, half, group), rows = num_pages * 64
+      const int64_t pages = kv->num_pages > 0 ? kv->num_pages : (int64_t)batch * kv->max_pages;
+      const uint64_t dims[4] = {64, (uint64_t)(pages * kB), 2, (uint64_t)cfg->h_kv};
+      const uint64_t str[3] = {(uint64_t)cfg->h_kv * kD * 2, 128, (uint64_t)kD * 2};
+      const uint32_t box[4] = {64, (uint32_t)kDStageKeys, 2, 1};
+      if (!make_tmap_bf16(&maps.k, kv->k_pages, 4, dims, str, box) ||
+          !make_tmap_bf16(&maps.v, kv->v_pages, 4, dims, str, box)) {
+        set_error("cuTensorMapEncodeTiled(page pools) failed");
+        return SWATTN_ECUDA;
+      }
+    }
     decode_attn_mma_kernel<<<(units + kDW - 1) / kDW, kDW * 32, smem, st>>>(a, topk, cnt, po, pml,
-                                                                           D.attn_splits);
+                                                                           D.attn_splits, maps);
     SWATTN_LAUNCH_CHECK("decode_attn_mma_kernel");
   }
-  decode_combine_kernel<<<nrows, 512, 0, st>>>(a, cnt, po, pml, D.attn_splits,
+  decode_combine_kernel<<<dim3(nrows, kG / 4), 128, 0, st>>>(a, cnt, po, pml, D.attn_splits,
                                                static_cast<__nv_bfloat16 *>(o), lse);
   SWATTN_LAUNCH_CHECK("decode_combine_kernel");
   return SWATTN_OK;

@@ -73,6 +73,7 @@ class PagedKVCache:
         kv.kc2 = self.kc2.data_ptr()
         kv.max_m1 = self.max_m1
         kv.max_m2 = self.max_m2
+        kv.num_pages = self.num_pages
         return kv
 
     def append(self, seq: int, K: torch.Tensor, V: torch.Tensor):

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the step in a CUDA graph and time graph replays")
     args = ap.parse_args()
     cfg = AttentionConfig()
     B, L = args.batch, args.ctx
@@ -60,12 +62,29 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    run = step
+    if args.graph:
+        # the step's seven launches (+ one memset) replayed as one graph:
+        # no per-launch host overhead or inter-kernel launch gaps
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(graph, stream=gs):
+                _lib.check(Lb.swattn_decode_step(c, kv, q.data_ptr(), B, o.data_ptr(), lse.data_ptr(),
+                                                 topk.data_ptr(), ws.data_ptr(), nbytes,
+                                                 torch.cuda.current_stream().cuda_stream), "decode")
+        stream.wait_stream(gs)
+        torch.cuda.synchronize()
+        run = graph.replay
+        run()
+        torch.cuda.synchronize()
     times = []
     for _ in range(args.steps):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        step()
+        run()
         b.record(stream)
         torch.cuda.synchronize()
         times.append(a.elapsed_time(b))
@@ -112,6 +131,7 @@ def main():
             "value": B / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms, "steps": args.steps,
             "higher_is_better": True, "dtype": "bf16", "data": "synthetic (torch.randn K/V/q, seeded)",
             "config": {"workload": f"decode batch {B}, context {L}, paged (64-token pages, shuffled pool)",
+                       "launch": "CUDA graph replay" if args.graph else "eager launches",
                        "l2": "flushed between steps (256 MB write)"},
             "roofline": {"bound": "hbm", "achieved": bytes_step / (ms / 1e3) / 1e9, "peak": hbm,
                          "unit": "GB/s", "frac": bytes_step / (ms / 1e3) / 1e9 / hbm,
