@@ -51,6 +51,33 @@ struct Dims {
   int h_q, h_kv, d;
 };
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Chains of small dependent kernels (the decode step) launch each kernel
+// with cudaLaunchAttributeProgrammaticStreamSerialization: it is scheduled
+// while its predecessor drains, runs its prologue (smem / barrier setup,
+// loads of step inputs), and blocks in pdl_wait() -- griddepcontrol.wait:
+// the predecessor grid has completed and its writes are visible -- before
+// it reads the predecessor's outputs.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- small device helpers
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
 

@@ -111,7 +111,7 @@ __device__ __forceinline__ void mma16816_p1(float (&c)[4], const uint32_t (&a)[4
 // (cp.async, double buffer) while the current one is scored from shared
 // memory (ldmatrix); one (max, sum) partial per slice and head, merged in
 // the same order as before (n-tiles of a lane, the lane quad, the 4 warps).
-constexpr int kP1Ctas = 8;
+constexpr int kP1Ctas = 13;  // 416 CTAs at batch 16: one wave at 3 CTAs per SM
 
 __device__ __forceinline__ void p1_issue_slice(uint32_t kt, const __nv_bfloat16 *kbase, int64_t col0,
                                                int64_t vis, int h_kv) {
@@ -128,10 +128,14 @@ __device__ __forceinline__ void p1_issue_slice(uint32_t kt, const __nv_bfloat16 
   asm volatile("cp.async.commit_group;");
 }
 
-__global__ void __launch_bounds__(128) decode_pass1_kernel(DecodeArgs a, float2 *part, int splits) {
+__global__ void __launch_bounds__(128) decode_pass1_kernel(DecodeArgs a, float2 *part, int splits,
+                                                           int32_t *amb_count) {
   extern __shared__ uint8_t p1_raw[];
   uint8_t *ktiles = p1_raw + ((128u - (tc::smem_u32(p1_raw) & 127u)) & 127u);  // [2][128 rows][256 B]
   __shared__ float2 red[4][kG];
+  pdl_launch_dependents();
+  // the step's flagged-row counter (read by top-k / re-rank after pass 2)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *amb_count = 0;
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
   const int64_t vis2 = vis_count(L - 1, a.l_C2, a.s_C2);
@@ -251,7 +255,7 @@ __device__ __forceinline__ unsigned long long spread_bits2(uint32_t x) {  // bit
 // (cp.async, double buffer) while the current one is scored, and merges the
 // row's pass-1 partials and loads q once (a CTA per tile repeated both 67
 // times per row and ran 2.4 short waves: 26-31 us, profiles/r02k).
-constexpr int kP2Ctas = 8;
+constexpr int kP2Ctas = 13;
 
 __device__ __forceinline__ void p2_issue_tile(uint32_t kt, const __nv_bfloat16 *kbase, int64_t tile0,
                                               int64_t vis1, int h_kv) {
@@ -290,6 +294,22 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
   const __nv_bfloat16 *kbase = a.kc1 + ((int64_t)seq * a.max_m1 * a.h_kv + g) * kD;
   const uint32_t kt0 = tc::smem_u32(ktiles);
   p2_issue_tile(kt0, kbase, (int64_t)blockIdx.y * kTileBlocks * kPoolS, vis1, a.h_kv);
+  pdl_launch_dependents();
+  // q as A fragments (a step input): a0 = (head r, d k), a1 = (r + 8, k), a2 = (r, k + 8), a3 = (r + 8, k + 8)
+  const int r = lane >> 2, dw = lane & 3;
+  uint32_t qa[8][4];
+  {
+    const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.q + (((int64_t)seq * a.h_q + g * kG + r) * kD));
+    const uint32_t *q1 = q0 + 8 * (kD / 2);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qa[ks][0] = __ldg(q0 + ks * 8 + dw);
+      qa[ks][1] = __ldg(q1 + ks * 8 + dw);
+      qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
+      qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
+    }
+  }
+  pdl_wait();  // pass-1 partials
   if (warp == 0) {
     // pass-1 partials of this row: only the slices pass 1 covered hold data
     // (C2 columns for approx rows, C1 for fallback rows); lane pairs (h, half)
@@ -320,18 +340,6 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
     if (Mt != -INFINITY)
       St = (M == -INFINITY ? 0.f : S * fast_exp2(M - Mt)) + (oM == -INFINITY ? 0.f : oS * fast_exp2(oM - Mt));
     if (half == 0) stat[h] = make_float2(Mt == -INFINITY ? 0.f : Mt, St > 0.f ? 1.f / St : 0.f);
-  }
-  // q as A fragments: a0 = (head r, d k), a1 = (r + 8, k), a2 = (r, k + 8), a3 = (r + 8, k + 8)
-  const int r = lane >> 2, dw = lane & 3;
-  const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.q + (((int64_t)seq * a.h_q + g * kG + r) * kD));
-  const uint32_t *q1 = q0 + 8 * (kD / 2);
-  uint32_t qa[8][4];
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-    qa[ks][0] = __ldg(q0 + ks * 8 + dw);
-    qa[ks][1] = __ldg(q1 + ks * 8 + dw);
-    qa[ks][2] = __ldg(q0 + ks * 8 + 4 + dw);
-    qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
   }
   const int lm = lane >> 3, lr = lane & 7;
   int buf = 0;
@@ -479,6 +487,8 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
     tc::fence_barrier_init();
   }
   __syncwarp();
+  pdl_launch_dependents();
+  pdl_wait();  // top-k (and its re-rank)
   const int row = unit / splits, split = unit % splits;
   const int seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
@@ -636,6 +646,7 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeArgs a, const
                                                              __nv_bfloat16 *o, float *lse) {
   const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
   const int h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  pdl_wait();  // the attention partials
   const int64_t L = a.seq_lens[seq];
   if (L < 1) {  // empty slot: defined outputs (O = 0, lse = -inf), nothing read
     o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 0] = __float2bfloat16_rn(0.f);
@@ -835,7 +846,7 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
       cudaFuncSetAttribute(decode_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2Smem);
       attr = true;
     }
-    decode_pass1_kernel<<<dim3(nrows, kP1Ctas), 128, kP2Smem, st>>>(a, p1, D.p1_splits);
+    decode_pass1_kernel<<<dim3(nrows, kP1Ctas), 128, kP2Smem, st>>>(a, p1, D.p1_splits, count);
   }
   SWATTN_LAUNCH_CHECK("decode_pass1_kernel");
   uint64_t *flags = reinterpret_cast<uint64_t *>(ws + D.off_flags);
@@ -845,11 +856,10 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
       cudaFuncSetAttribute(decode_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2Smem);
       attr = true;
     }
-    decode_pass2_kernel<<<dim3(nrows, kP2Ctas), 128, kP2Smem, st>>>(a, p1, D.p1_splits, scmp, D.ld,
-                                                                   flags, D.tiles);
+    launch_pdl(decode_pass2_kernel, dim3(nrows, kP2Ctas), dim3(128), kP2Smem, st, a, p1, D.p1_splits,
+               scmp, D.ld, flags, D.tiles);
   }
   SWATTN_LAUNCH_CHECK("decode_pass2_kernel");
-  if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset"))) return rc;
   if ((rc = launch_decode_topk(cfg, scmp, D.ld, kv->seq_lens, batch, D.max_ctx, topk, cnt, count,
                                rows, nrows, flags, D.tiles, st)))
     return rc;
@@ -878,12 +888,12 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
         return SWATTN_ECUDA;
       }
     }
-    decode_attn_mma_kernel<<<(units + kDW - 1) / kDW, kDW * 32, smem, st>>>(a, topk, cnt, po, pml,
-                                                                           D.attn_splits, maps);
+    launch_pdl(decode_attn_mma_kernel, dim3((units + kDW - 1) / kDW), dim3(kDW * 32), smem, st, a,
+               (const int32_t *)topk, (const int32_t *)cnt, po, pml, D.attn_splits, maps);
     SWATTN_LAUNCH_CHECK("decode_attn_mma_kernel");
   }
-  decode_combine_kernel<<<dim3(nrows, kG / 4), 128, 0, st>>>(a, cnt, po, pml, D.attn_splits,
-                                               static_cast<__nv_bfloat16 *>(o), lse);
+  launch_pdl(decode_combine_kernel, dim3(nrows, kG / 4), dim3(128), 0, st, a, (const int32_t *)cnt,
+             (const float *)po, (const float2 *)pml, D.attn_splits, static_cast<__nv_bfloat16 *>(o), lse);
   SWATTN_LAUNCH_CHECK("decode_combine_kernel");
   return SWATTN_OK;
 }

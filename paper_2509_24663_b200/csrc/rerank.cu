@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_p1_kernel(RerankArgs a) {
   __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
   __shared__ double mh[kG], lh[kG];
   extern __shared__ __nv_bfloat16 kc_s[];  // [kD][kChunk]
+  pdl_launch_dependents();
+  pdl_wait();  // flagged rows come from the top-k kernel
   const int total = min(*a.count, a.cap);
   if (total > kSplitRows || a.partials == nullptr) return;
   for (int w = blockIdx.x; w < total * kP1Split; w += gridDim.x) {
@@ -206,6 +208,8 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
   __shared__ int n_members, n_above;
 
   __shared__ double mh[kG], lh[kG];
+  pdl_launch_dependents();
+  pdl_wait();  // flagged rows / pass-1 partials from the preceding kernels
   const int total = min(*a.count, a.cap);
   const bool split = total <= kSplitRows && a.partials != nullptr;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -373,12 +377,19 @@ int32_t run_rerank(const RerankArgs &a, int num_sms, cudaStream_t stream) {
     cudaFuncSetAttribute(rerank_p1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  // decode: programmatic dependent launches (see launch_pdl, common.cuh)
   if (a.partials != nullptr) {
     // no-op unless at most kSplitRows rows were flagged (decided on the device)
-    rerank_p1_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);
+    if (a.decode)
+      launch_pdl(rerank_p1_kernel, dim3(num_sms * 2), dim3(kThreads), smem, stream, a);
+    else
+      rerank_p1_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);
     SWATTN_LAUNCH_CHECK("rerank_p1_kernel");
   }
-  rerank_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);  // 2 CTAs per SM (launch bounds)
+  if (a.decode)
+    launch_pdl(rerank_kernel, dim3(num_sms * 2), dim3(kThreads), smem, stream, a);
+  else
+    rerank_kernel<<<num_sms * 2, kThreads, smem, stream>>>(a);  // 2 CTAs per SM (launch bounds)
   SWATTN_LAUNCH_CHECK("rerank_kernel");
   return SWATTN_OK;
 }

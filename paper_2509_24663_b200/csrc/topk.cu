@@ -549,6 +549,8 @@ decode_topk_cta_kernel(const float *__restrict__ s_cmp, int64_t ld, const int32_
   __shared__ int wsum[kDecThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t row = blockIdx.x;  // seq * h_kv + g
+  pdl_launch_dependents();
+  pdl_wait();  // S^cmp and the tie flags from decode pass 2
   const int L = seq_lens[row / h_kv];
   const int64_t i = L - 1;
   const int64_t m1 = num_pooled(L, l_C1, s_C1);
@@ -802,9 +804,9 @@ int32_t launch_decode_topk(const swattn_config *cfg, const float *s_cmp, int64_t
   if (cfg->k_top <= 0) return SWATTN_OK;
   const int64_t rows = (int64_t)cfg->h_kv * batch;
   AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
-  decode_topk_cta_kernel<<<(unsigned)rows, kDecThreads, 0, stream>>>(
-      s_cmp, ld, seq_lens, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, cfg->l_C1,
-      cfg->s_C1, cfg->s, topk, topk_cnt, amb);
+  launch_pdl(decode_topk_cta_kernel, dim3((unsigned)rows), dim3(kDecThreads), 0, stream, s_cmp, ld,
+             seq_lens, cfg->h_kv, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, cfg->l_C1, cfg->s_C1,
+             cfg->s, topk, topk_cnt, amb);
   SWATTN_LAUNCH_CHECK("decode_topk_kernel");
   return SWATTN_OK;
 }
