@@ -270,6 +270,11 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv,
                            void *stream);
 size_t swattn_decode_workspace_bytes(const swattn_config *cfg, int32_t batch,
                                      int32_t max_pages);
+/* Diagnostics: byte offset in the decode workspace of the int32 count of
+ * (sequence, group) rows the last swattn_decode_step settled by the float64
+ * boundary re-rank (valid after the step completes; -1 on bad arguments). */
+int64_t swattn_decode_reranked_offset(const swattn_config *cfg, int32_t batch,
+                                      int32_t max_pages);
 
 #ifdef __cplusplus
 }

@@ -781,6 +781,11 @@ size_t swattn_decode_workspace_bytes(const swattn_config *cfg, int32_t batch, in
   return decode_layout(cfg, batch, max_pages).total;
 }
 
+int64_t swattn_decode_reranked_offset(const swattn_config *cfg, int32_t batch, int32_t max_pages) {
+  if (cfg == nullptr || batch < 1 || max_pages < 1) return -1;
+  return (int64_t)decode_layout(cfg, batch, max_pages).off_count;
+}
+
 static int32_t check_decode(const swattn_config *cfg, const swattn_paged_kv *kv, int32_t batch) {
   int32_t rc = swattn_validate_config(cfg);
   if (rc) return rc;

@@ -30,12 +30,13 @@ def main():
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graph", action="store_true",
                     help="capture the step in a CUDA graph and time graph replays")
     args = ap.parse_args()
     cfg = AttentionConfig()
     B, L = args.batch, args.ctx
-    g = torch.Generator(device="cuda").manual_seed(0)
+    g = torch.Generator(device="cuda").manual_seed(args.seed)
     cache = PagedKVCache(cfg, batch=B, max_pages=-(-L // cfg.B) + 1, seed=3)
     for b in range(B):
         K = torch.randn((L, cfg.h_kv, cfg.d_h), generator=g, device="cuda").to(torch.bfloat16)
@@ -89,6 +90,8 @@ def main():
         torch.cuda.synchronize()
         times.append(a.elapsed_time(b))
     ms = float(np.median(times))
+    off = Lb.swattn_decode_reranked_offset(c, B, cache.max_pages)
+    reranked = int(ws[off:off + 4].view(torch.int32).item())
     # dense decode comparator: flash-attn 2.8 decode over the same 16 x 128K
     # contexts held contiguously (its paged path needs 256-token pages)
     dense = {}
@@ -136,6 +139,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": bytes_step / (ms / 1e3) / 1e9, "peak": hbm,
                          "unit": "GB/s", "frac": bytes_step / (ms / 1e3) / 1e9 / hbm,
                          "algorithmic_bytes_per_step": bytes_step},
+            "rows_reranked_per_step": reranked,
             "dense_decode_comparator": dense}
     if "ms" in dense:
         line["speedup_vs_dense_decode"] = dense["ms"] / ms
