@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "topk_cta.cuh"
 
 namespace swattn {
 
@@ -48,7 +49,10 @@ int32_t launch_scores_simt(const swattn_config *, const void *, const void *, co
                            int32_t, float *, int64_t, uint64_t *, int64_t, cudaStream_t);
 int32_t launch_scores_tc(const swattn_config *, const void *, const void *, const void *, int64_t,
                          int64_t, int64_t, int32_t, float *, int64_t, uint64_t *, int64_t,
-                         cudaStream_t);
+                         cudaStream_t, const FusedTopk *fz = nullptr);
+int32_t launch_topk_tail(const swattn_config *, const float *, int64_t, int64_t, int64_t, int64_t,
+                         int32_t *, int32_t *, int32_t *, int32_t *, int32_t, const uint64_t *, int64_t,
+                         const int32_t *, const int32_t *, cudaStream_t);
 int32_t launch_shared_scores(const swattn_config *, const void *, const void *, const void *,
                              int64_t, int32_t, float *, uint8_t *, float *, cudaStream_t);
 int32_t launch_maxpool(const swattn_config *, const float *, int64_t, float *, int64_t,
@@ -120,8 +124,8 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SelectLayout {
   int64_t m1, m2, n_cols, ld, ld_f;
-  size_t off_kc1, off_kc2, off_scmp, off_flags, off_count, off_rows, off_part, off_shared, off_lse,
-      total;
+  size_t off_kc1, off_kc2, off_scmp, off_flags, off_count, off_rows, off_ovf, off_part, off_shared,
+      off_lse, total;
   bool generic;
 };
 
@@ -142,6 +146,8 @@ static SelectLayout select_layout(const swattn_config *cfg, int64_t n) {
   L.off_count = o; o = align_up(o + 16);
   // flagged row ids [cap] followed by their k-th keys [cap] (K3 -> re-rank)
   L.off_rows = o; o = align_up(o + (size_t)cfg->h_kv * n * 4 * 2);
+  // rows whose fused top-k candidate set overflowed (K2 -> topk_tail_kernel)
+  L.off_ovf = o; o = align_up(o + (size_t)cfg->h_kv * n * 4);
   L.off_part = o; o = align_up(o + rerank_partials_bytes());
   L.off_shared = o;
   if (L.generic) o = align_up(o + (size_t)n * cfg->h_kv * L.m1 * 4);
@@ -405,17 +411,40 @@ static int32_t select_rows(const swattn_config *cfg, const void *Q, const void *
     if (n_reranked) cudaMemsetAsync(n_reranked, 0, 4, st);
     return rc;
   }
-  if (use_tc_scores())
-    rc = launch_scores_tc(cfg, Q, kc1, kc2, n, r0, r1, mode, scmp, L.ld, flags, L.ld_f, st);
-  else
-    rc = launch_scores_simt(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
-  if (rc) return rc;
-  if (after_scores != nullptr && (rc = after_scores->run(st))) return rc;
-  if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset(count)"))) return rc;
   const int32_t cap = (int32_t)((int64_t)cfg->h_kv * n);
-  if ((rc = launch_topk(cfg, scmp, L.ld, n, r0, r1, topk, topk_cnt, count, rows, cap, flags,
-                        L.ld_f, st)))
-    return rc;
+  // Row f1 (opt-in, SWATTN_K2_TOPK=1): the top-k selected in K2's pass-2
+  // epilogue (scores_tc.cu); K3 then only fills rows without candidates and
+  // re-selects rows whose candidate set overflowed.  Bit-identical selections,
+  // but K2 is co-bound by issue slots and MUFU and its 8 epilogue warps meet
+  // at a barrier every tile, so the per-token candidate maintenance costs more
+  // than the separate 1.1 ms K3 (128K select 14.0 vs 10.4 ms,
+  // profiles/r02ae_fused_topk.txt): off by default.
+  const char *fuse_e = getenv("SWATTN_K2_TOPK");
+  const bool fuse_env = fuse_e != nullptr && strcmp(fuse_e, "1") == 0;
+  const bool fused = fuse_env && use_tc_scores() && cfg->k_top > 0 && cfg->k_top <= 64 &&
+                     L.n_cols - cfg->N_init <= kTopkMaxCand;
+  if (fused) {
+    int32_t *ovf_rows = reinterpret_cast<int32_t *>(ws + L.off_ovf);
+    if ((rc = cuda_check(cudaMemsetAsync(count, 0, 8, st), "memset(count)"))) return rc;
+    const FusedTopk fz{topk, topk_cnt, count, rows, cap, count + 1, ovf_rows};
+    if ((rc = launch_scores_tc(cfg, Q, kc1, kc2, n, r0, r1, mode, scmp, L.ld, flags, L.ld_f, st, &fz)))
+      return rc;
+    if (after_scores != nullptr && (rc = after_scores->run(st))) return rc;
+    if ((rc = launch_topk_tail(cfg, scmp, L.ld, n, r0, r1, topk, topk_cnt, count, rows, cap, flags,
+                               L.ld_f, count + 1, ovf_rows, st)))
+      return rc;
+  } else {
+    if (use_tc_scores())
+      rc = launch_scores_tc(cfg, Q, kc1, kc2, n, r0, r1, mode, scmp, L.ld, flags, L.ld_f, st);
+    else
+      rc = launch_scores_simt(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, flags, L.ld_f, st);
+    if (rc) return rc;
+    if (after_scores != nullptr && (rc = after_scores->run(st))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(count, 0, 4, st), "memset(count)"))) return rc;
+    if ((rc = launch_topk(cfg, scmp, L.ld, n, r0, r1, topk, topk_cnt, count, rows, cap, flags,
+                          L.ld_f, st)))
+      return rc;
+  }
   if ((rc = launch_rerank(cfg, Q, kc1, kc2, n, mode, scmp, L.ld, count, rows, cap, topk,
                           ws + L.off_part, num_sms(), st)))
     return rc;

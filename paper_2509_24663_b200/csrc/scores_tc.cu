@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "tc.cuh"
 #include "tma_host.cuh"
+#include "topk_cta.cuh"
 
 namespace swattn {
 
@@ -80,7 +81,20 @@ struct ScParams {
   int64_t ld;
   uint64_t *flags;
   int64_t ld_f;
+  // top-k in the pass-2 epilogue (row f1; null topk = S^cmp only, K3 selects)
+  int32_t *topk, *topk_cnt;
+  int k_top;
+  AmbList amb;
+  int32_t *ovf_count, *ovf_rows;  // rows whose candidate set overflowed (massive ties)
 };
+
+// Per-token running candidate set of the fused top-k: every block score of
+// a tile that reaches the token's threshold is appended (ballot) in block
+// order; when the next tile might not fit, the set is compacted to the keys
+// >= (k-th largest) x (1 - 4 eps), which keeps the final top-k, every key
+// within the float32 error band below the final k-th, and every key above
+// it (the threshold only rises, and stays below the final k-th by 4 eps).
+constexpr int kCand = 128;
 
 struct __align__(1024) ScSmem {
   uint8_t q[kQBytes];
@@ -89,8 +103,25 @@ struct __align__(1024) ScSmem {
   __align__(16) float2 stat[kRows];  // (m, 1/l) per (token, head) row, log2 domain
   float2 stat_hi[kRows];             // warpgroup 1's pass-1 (m, l) before the merge
   float sc[kTok][kCols + 4];   // tile column scores for the max-pool
+  uint32_t ckey[kTok][kCand];  // fused top-k: candidate keys (f2key of S^cmp), block order
+  uint16_t cid[kTok][kCand];   //   and their block ids
   uint32_t tmem_base;
 };
+
+// k-th largest of the warp's candidate keys (lane holds entries lane + 32 e;
+// invalid entries are 0): the largest X with #{key >= X} >= k, bit by bit
+__device__ __forceinline__ uint32_t warp_kth_key(const uint32_t (&kv)[kCand / 32], int k) {
+  uint32_t x = 0u;
+#pragma unroll 1
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t c = x | (1u << bit);
+    int n = 0;
+#pragma unroll
+    for (int e = 0; e < kCand / 32; ++e) n += kv[e] >= c;
+    if (__reduce_add_sync(0xffffffffu, n) >= k) x = c;
+  }
+  return x;
+}
 
 // bit q of x -> bit 2q of the result (Morton spread)
 __device__ __forceinline__ unsigned long long spread_bits(uint32_t x) {
@@ -254,6 +285,12 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
     // No causal / edge masking is needed here: every column of a candidate
     // block's window (cols <= 4*hi) is visible to all 8 rows (vis1 >= 4b - 1)
     // and < m1; values of other columns are never written.
+    const bool fuse = p.topk != nullptr;
+    const int ksel = min(p.k_top, max(hi - p.N_init, 0));  // the same for the CTA's 8 tokens
+    int ccnt = 0;          // fused top-k state of token warp - 2 (warp-uniform)
+    uint32_t cthr = 0u;
+    bool covf = false;
+    uint32_t t1 = 0u, t2 = 0u, t3 = 0u;  // this lane's 3 largest keys so far
     for (int t = 0; t < n_t2; ++t) {
       const int u = n_c1 + t;
       const int tb = u & 1;
@@ -311,6 +348,83 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
         for (int e = 0; e < kPoolL; ++e) v[e] = s.sc[k][min(qb * kPoolS + e, kCols - 1)];
         const float mx = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), v[4]);
         if (ok) p.s_cmp[((int64_t)g * p.n + tok) * p.ld + j] = mx;
+        if (fuse && !covf) {
+          // threshold: every lane holds >= 3 keys >= its 3rd largest, so >= 93
+          // keys are >= tau = the lanes' minimum, and the final top-k is above
+          // it; appending / keeping keys >= tau (1 - 4 eps) also keeps the
+          // float32 error band below the final k-th.  Compaction is then one
+          // ordered stream-compaction pass (no k-th search in the tile loop).
+          const uint32_t key = ok ? f2key(mx) : 0u;
+          if (key > t3) {
+            if (key > t1) { t3 = t2; t2 = t1; t1 = key; }
+            else if (key > t2) { t3 = t2; t2 = key; }
+            else t3 = key;
+          }
+          const uint32_t tau = __reduce_min_sync(0xffffffffu, lane < kTileBlocks ? t3 : 0xffffffffu);
+          if (tau != 0u) cthr = max(cthr, f2key(key2f(tau) * (1.f - 4.f * kScoreRelErr)));
+          if (ccnt + kTileBlocks > kCand) {
+            uint32_t kv[kCand / 32];
+            uint16_t iv[kCand / 32];
+#pragma unroll
+            for (int e = 0; e < kCand / 32; ++e) {
+              const int q = e * 32 + lane;
+              kv[e] = q < ccnt ? s.ckey[k][q] : 0u;
+              iv[e] = q < ccnt ? s.cid[k][q] : (uint16_t)0;
+            }
+            __syncwarp();
+            int w = 0;
+#pragma unroll
+            for (int e = 0; e < kCand / 32; ++e) {
+              const bool keep = kv[e] >= cthr && kv[e] != 0u;
+              const unsigned km = __ballot_sync(0xffffffffu, keep);
+              if (keep) {
+                const int pos = w + __popc(km & ((1u << lane) - 1u));
+                s.ckey[k][pos] = kv[e];
+                s.cid[k][pos] = iv[e];
+              }
+              w += __popc(km);
+            }
+            ccnt = w;
+            __syncwarp();
+            if (ccnt + kTileBlocks > kCand) {
+              // the lane bound was too loose: raise the threshold to the exact
+              // k-th largest x (1 - 4 eps) and compact again (a few times per row)
+#pragma unroll
+              for (int e = 0; e < kCand / 32; ++e) {
+                const int q = e * 32 + lane;
+                kv[e] = q < ccnt ? s.ckey[k][q] : 0u;
+                iv[e] = q < ccnt ? s.cid[k][q] : (uint16_t)0;
+              }
+              const uint32_t T = warp_kth_key(kv, ksel);
+              cthr = max(cthr, f2key(key2f(T) * (1.f - 4.f * kScoreRelErr)));
+              __syncwarp();
+              w = 0;
+#pragma unroll
+              for (int e = 0; e < kCand / 32; ++e) {
+                const bool keep = kv[e] >= cthr && kv[e] != 0u;
+                const unsigned km = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                  const int pos = w + __popc(km & ((1u << lane) - 1u));
+                  s.ckey[k][pos] = kv[e];
+                  s.cid[k][pos] = iv[e];
+                }
+                w += __popc(km);
+              }
+              ccnt = w;
+              __syncwarp();
+            }
+            covf = ccnt + kTileBlocks > kCand;  // massive ties: the fallback selects from S^cmp
+          }
+          const bool take = ok && !covf && key >= cthr;
+          const unsigned tm = __ballot_sync(0xffffffffu, take);
+          if (take) {
+            const int pos = ccnt + __popc(tm & ((1u << lane) - 1u));
+            s.ckey[k][pos] = key;
+            s.cid[k][pos] = (uint16_t)j;
+          }
+          ccnt += __popc(tm);
+          __syncwarp();
+        }
         if (p.flags != nullptr) {
           // argmax-at-shared-column bits (L: window col 0, R: col 4) with margin
           const float f = 1.f + 4.f * kScoreRelErr;
@@ -324,6 +438,93 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");  // s.sc reuse by the next tile
     }
+    if (fuse) {
+      // ---- the token's selection from its candidate set (as K3 from S^cmp,
+      // topk.cu / topk_cta.cuh: keys > T, then keys == T by ascending block
+      // index, emitted ascending; the same float32 ambiguity test)
+      const int k = warp - 2;
+      const int64_t tok = i0 + k;
+      if (tok < p.r1) {
+        const int64_t row = (int64_t)g * p.n + tok;
+        int32_t *out = p.topk + row * p.k_top;
+        if (lane == 0) p.topk_cnt[row] = ksel;
+        if (covf) {
+          if (lane == 0) p.ovf_rows[atomicAdd(p.ovf_count, 1)] = (int32_t)row;
+        } else {
+          uint32_t kv[kCand / 32];
+          uint16_t iv[kCand / 32];
+#pragma unroll
+          for (int e = 0; e < kCand / 32; ++e) {
+            const int q = e * 32 + lane;
+            kv[e] = q < ccnt ? s.ckey[k][q] : 0u;
+            iv[e] = q < ccnt ? s.cid[k][q] : (uint16_t)0;
+          }
+          const bool all = ksel >= max(hi - p.N_init, 0);  // every candidate: no ranking
+          const uint32_t T = all ? 0u : warp_kth_key(kv, ksel);
+          int gt = 0, eq = 0;
+          uint32_t below = 0u, above = 0xffffffffu;
+#pragma unroll
+          for (int e = 0; e < kCand / 32; ++e) {
+            if (kv[e] == 0u) continue;
+            if (kv[e] > T) { ++gt; above = min(above, kv[e]); }
+            else if (kv[e] == T) ++eq;
+            else below = max(below, kv[e]);
+          }
+          gt = __reduce_add_sync(0xffffffffu, gt);
+          eq = __reduce_add_sync(0xffffffffu, eq);
+          below = __reduce_max_sync(0xffffffffu, below);
+          above = __reduce_min_sync(0xffffffffu, above);
+          const int need_eq = ksel - gt;
+          int written = 0, eq_seen = 0, first = -1, second = -1;
+#pragma unroll
+          for (int e = 0; e < kCand / 32; ++e) {
+            const bool valid = kv[e] != 0u;
+            const bool is_eq = valid && kv[e] == T && !all;
+            const unsigned em = __ballot_sync(0xffffffffu, is_eq);
+            const int eq_rank = eq_seen + __popc(em & ((1u << lane) - 1u));
+            const bool tk = valid && (all || kv[e] > T || (is_eq && eq_rank < need_eq));
+            const unsigned tkm = __ballot_sync(0xffffffffu, tk);
+            if (tk) out[written + __popc(tkm & ((1u << lane) - 1u))] = iv[e];
+            written += __popc(tkm);
+            // the first two tied ids (ascending: buffer order)
+            unsigned x = em;
+            while (x && second < 0) {
+              const int src = __ffs(x) - 1;
+              x &= x - 1;
+              const int id = __shfl_sync(0xffffffffu, (int)iv[e], src);
+              if (first < 0) first = id; else second = id;
+            }
+            eq_seen += __popc(em);
+          }
+          for (int q = written + lane; q < p.k_top; q += 32) out[q] = -1;
+          if (!all && p.amb.count != nullptr) {
+            bool ambiguous;
+            if (gt + eq > ksel) {
+              ambiguous = true;
+              if (eq == 2 && p.amb.flags != nullptr && second == first + 1) {
+                const int jj = first;
+                const uint64_t *fr = p.amb.flags + row * p.amb.ld_f;
+                const int tj = jj / 31, qj = jj % 31, tj1 = (jj + 1) / 31, qj1 = (jj + 1) % 31;
+                const bool R_j = (fr[tj] >> (2 * qj + 1)) & 1ull;
+                const bool L_j1 = (fr[tj1] >> (2 * qj1)) & 1ull;
+                ambiguous = !(R_j && L_j1) || tie_neighbours_close(T, below, above);
+              }
+            } else {
+              const float vk = key2f(T);
+              const float vb = below ? key2f(below) : -INFINITY;
+              ambiguous = (vk - vb) <= 3.0f * kScoreRelErr * fabsf(vk);
+            }
+            if (ambiguous && lane == 0) {
+              const int slot = atomicAdd(p.amb.count, 1);
+              if (slot < p.amb.cap) {
+                p.amb.rows[slot] = (int32_t)row;
+                p.amb.rows[p.amb.cap + slot] = (int32_t)T;
+              }
+            }
+          }
+        }
+      }
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -336,9 +537,17 @@ bool scores_tc_available() { return true; }
 
 int32_t launch_scores_tc(const swattn_config *cfg, const void *Q, const void *kc1, const void *kc2,
                          int64_t n, int64_t r0, int64_t r1, int32_t mode, float *s_cmp, int64_t ld,
-                         uint64_t *flags, int64_t ld_f, cudaStream_t stream) {
+                         uint64_t *flags, int64_t ld_f, cudaStream_t stream, const FusedTopk *fz) {
   ScParams p;
   memset(&p, 0, sizeof(p));
+  if (fz != nullptr) {
+    p.topk = fz->topk;
+    p.topk_cnt = fz->topk_cnt;
+    p.k_top = cfg->k_top;
+    p.amb = AmbList{fz->amb_count, fz->amb_rows, fz->amb_cap, flags, ld_f};
+    p.ovf_count = fz->ovf_count;
+    p.ovf_rows = fz->ovf_rows;
+  }
   p.n = n;
   p.m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
   p.m2 = num_pooled(n, cfg->l_C2, cfg->s_C2);

@@ -16,6 +16,8 @@
 // ambiguous and resolve by index exactly as in float64.
 //
 // Roofline: HBM-bound; bytes = candidate S^cmp fp32 read + topk int32 write.
+#include <algorithm>
+
 #include "common.cuh"
 #include "topk_cta.cuh"
 
@@ -507,6 +509,37 @@ topk_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int64_t r0, 
                   keys_s + (size_t)warp * cand_stride, hist_s + warp * 256, amb, row);
 }
 
+// After the fused K2 (scores_tc.cu selects in its epilogue): rows [r0, t1)
+// without candidates get count 0 / ids -1, and the rows whose candidate set
+// overflowed (ovf list, usually empty) are selected here from S^cmp by the
+// staged generic path, with the same ambiguity recording as topk_kernel.
+__global__ void __launch_bounds__(kWarps * 32)
+topk_tail_kernel(const float *__restrict__ s_cmp, int64_t ld, int64_t n, int64_t r0, int64_t t1, int gc,
+                 int g0, int B, int N_init, int N_local, int k_top, int n_cols, int l_C1, int cand_stride,
+                 int32_t *__restrict__ topk, int32_t *__restrict__ topk_cnt, AmbList amb,
+                 const int32_t *__restrict__ ovf_count, const int32_t *__restrict__ ovf_rows) {
+  extern __shared__ uint32_t keys_s[];  // [kWarps][cand_stride]
+  __shared__ int hist_s[kWarps * 256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nfill = (int64_t)gc * (t1 > r0 ? t1 - r0 : 0);
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nfill; f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = (g0 + f / (t1 - r0)) * n + r0 + f % (t1 - r0);
+    topk_cnt[row] = 0;
+    for (int q = 0; q < k_top; ++q) topk[row * k_top + q] = -1;
+  }
+  const int novf = *ovf_count;
+  for (int it = blockIdx.x * kWarps + warp; it < novf; it += gridDim.x * kWarps) {
+    const int64_t row = ovf_rows[it];
+    const int64_t i = row % n;
+    const int hi = cand_hi((int)(i / B), N_local, n_cols);
+    const int ncand = hi > N_init ? hi - N_init : 0;
+    const int k = (i + 1) < l_C1 ? 0 : (ncand < k_top ? ncand : k_top);
+    if (lane == 0) topk_cnt[row] = k;
+    warp_topk_row(s_cmp + row * ld + N_init, ncand, k, N_init, k_top, topk + row * k_top,
+                  keys_s + (size_t)warp * cand_stride, hist_s + warp * 256, amb, row);
+  }
+}
+
 // decode: one 512-thread CTA per (sequence, group) row (topk_cta.cuh)
 constexpr int kDecThreads = 512;
 __global__ void __launch_bounds__(kDecThreads)
@@ -557,6 +590,32 @@ int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, in
         cfg->l_C1, cand_stride, topk, topk_cnt, amb);
   }
   SWATTN_LAUNCH_CHECK("topk_kernel");
+  return SWATTN_OK;
+}
+
+int32_t launch_topk_tail(const swattn_config *cfg, const float *s_cmp, int64_t ld, int64_t n, int64_t r0,
+                         int64_t r1, int32_t *topk, int32_t *topk_cnt, int32_t *amb_count,
+                         int32_t *amb_rows, int32_t amb_cap, const uint64_t *flags, int64_t ld_f,
+                         const int32_t *ovf_count, const int32_t *ovf_rows, cudaStream_t stream) {
+  const int64_t m1 = num_pooled(n, cfg->l_C1, cfg->s_C1);
+  const int n_cols = (int)(m1 ? cdiv(m1, cfg->s) : 0);
+  if (cfg->k_top <= 0 || r1 <= r0) return SWATTN_OK;
+  const GroupRange gr = group_range(cfg);
+  const int64_t tok0 = (int64_t)(cfg->N_init + cfg->N_local) * cfg->B;
+  const int64_t t1 = std::min(r1, std::max(tok0, r0));
+  AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
+  const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
+  const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(topk_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kWarps * kMaxCand * sizeof(uint32_t)));
+    attr = true;
+  }
+  topk_tail_kernel<<<148, kWarps * 32, smem, stream>>>(
+      s_cmp, ld, n, r0, t1, gr.gc, gr.g0, cfg->B, cfg->N_init, cfg->N_local, cfg->k_top, n_cols,
+      cfg->l_C1, cand_stride, topk, topk_cnt, amb, ovf_count, ovf_rows);
+  SWATTN_LAUNCH_CHECK("topk_tail_kernel");
   return SWATTN_OK;
 }
 

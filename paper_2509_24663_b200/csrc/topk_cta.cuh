@@ -18,6 +18,16 @@ namespace swattn {
 
 constexpr int kTopkMaxCand = 4096;  // per-row candidate bound (block ids < 4096 + N_init)
 
+// Outputs of K2 when it selects the top-k in its pass-2 epilogue (row f1):
+// rows whose candidate set overflowed (massive exact ties) are listed for
+// launch_topk_tail, which selects them from S^cmp.
+struct FusedTopk {
+  int32_t *topk, *topk_cnt;
+  int32_t *amb_count, *amb_rows;
+  int32_t amb_cap;
+  int32_t *ovf_count, *ovf_rows;
+};
+
 // A proven structural tie straddling the k-th boundary still needs the
 // float32 error-bound check against the nearest distinct keys on both sides
 // (the pair as a whole may belong above the next key up or below the next

@@ -82,6 +82,22 @@ def test_k1_pooled_keys_bit_exact(name):
         assert O.digest(_host_bits(k2[:m2])) == str(rec["c2_digest"])
 
 
+@pytest.mark.parametrize("name", PAPER_GOLDEN)
+def test_selection_topk_fused_in_k2(name, monkeypatch):
+    """Row f1 (opt-in SWATTN_K2_TOPK=1): the top-k selected in K2's pass-2
+    epilogue from a per-token candidate set gives the reference's selection,
+    including the float64 re-rank of the rows it flags."""
+    rec, prof, cfg, host, (Qd, Kd, Vd) = _load(name)
+    monkeypatch.setenv("SWATTN_K2_TOPK", "1")
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    torch.cuda.synchronize()
+    got = sel.topk.cpu().numpy().astype(np.int64)
+    want = rec["topk"].astype(np.int64)[:, :, :cfg.k_top]
+    bad = np.argwhere((got != want).any(axis=2))
+    assert bad.size == 0, f"{len(bad)} rows differ, first {bad[:5].tolist()}"
+    assert np.array_equal(sel.counts, rec["counts"].astype(np.int64))
+
+
 @pytest.mark.parametrize("name", PAPER_GOLDEN + SMALL_GOLDEN)
 def test_selection_bit_exact(name):
     rec, prof, cfg, host, (Qd, Kd, Vd) = _load(name)
