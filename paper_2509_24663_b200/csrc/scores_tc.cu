@@ -23,6 +23,7 @@
 // other warps wait on TMEM loads or the max-pool barrier.
 // Roofline: tensor + MUFU; FLOP = 2 * h_q * d * (pass-1 cols + pass-2 cols)
 // per row (bench.py:144-155).
+#include <stddef.h>
 #include <string.h>
 
 #include <algorithm>
@@ -103,9 +104,10 @@ struct __align__(1024) ScSmem {
   __align__(16) float2 stat[kRows];  // (m, 1/l) per (token, head) row, log2 domain
   float2 stat_hi[kRows];             // warpgroup 1's pass-1 (m, l) before the merge
   float sc[kTok][kCols + 4];   // tile column scores for the max-pool
-  uint32_t ckey[kTok][kCand];  // fused top-k: candidate keys (f2key of S^cmp), block order
-  uint16_t cid[kTok][kCand];   //   and their block ids
   uint32_t tmem_base;
+  // fused top-k only (the default kernel is launched without these 6 KB):
+  uint32_t ckey[kTok][kCand];  // candidate keys (f2key of S^cmp), block order
+  uint16_t cid[kTok][kCand];   //   and their block ids
 };
 
 // k-th largest of the warp's candidate keys (lane holds entries lane + 32 e;
@@ -134,6 +136,9 @@ __device__ __forceinline__ unsigned long long spread_bits(uint32_t x) {
   return v;
 }
 
+// kFuse: row f1 variant (top-k in the pass-2 epilogue); compiled separately
+// so the default kernel carries none of its code
+template <bool kFuse>
 __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_constant__ ScParams p) {
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on smem_raw so accesses stay in the shared space
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2) scores_tc_kernel(const __grid_con
     // No causal / edge masking is needed here: every column of a candidate
     // block's window (cols <= 4*hi) is visible to all 8 rows (vis1 >= 4b - 1)
     // and < m1; values of other columns are never written.
-    const bool fuse = p.topk != nullptr;
+    constexpr bool fuse = kFuse;
     const int ksel = min(p.k_top, max(hi - p.N_init, 0));  // the same for the CTA's 8 tokens
     int ccnt = 0;          // fused top-k state of token warp - 2 (warp-uniform)
     uint32_t cthr = 0u;
@@ -598,16 +603,20 @@ int32_t launch_scores_tc(const swattn_config *cfg, const void *Q, const void *kc
       p.k2_map = p.k1_map;
     }
   }
-  const size_t smem = sizeof(ScSmem) + 1024;
+  const size_t smem_f = sizeof(ScSmem) + 1024, smem = offsetof(ScSmem, ckey) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(scores_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(scores_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(scores_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
     attr = true;
   }
   const GroupRange gr = group_range(cfg);
   p.g0 = gr.g0;
   dim3 grid((unsigned)p.n_tiles_tok, (unsigned)gr.gc);
-  scores_tc_kernel<<<grid, kThreads, smem, stream>>>(p);
+  if (p.topk != nullptr)
+    scores_tc_kernel<true><<<grid, kThreads, smem_f, stream>>>(p);
+  else
+    scores_tc_kernel<false><<<grid, kThreads, smem, stream>>>(p);
   SWATTN_LAUNCH_CHECK("scores_tc_kernel");
   return SWATTN_OK;
 }
