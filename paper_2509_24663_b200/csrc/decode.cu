@@ -42,7 +42,6 @@ constexpr int kP1Cols = 128;     // normaliser columns per pass-1 CTA (4 warps x
 constexpr int kTileBlocks = 31;  // pass-2 tile: 31 blocks, 124 (+4) columns
 constexpr int kTileCols = 128;
 constexpr int kP2Smem = 2 * kTileCols * 256 + 1024;  // passes 1 and 2: two 128-row key tiles
-constexpr int kAttnBlocks = 3;   // visible blocks per split-KV warp (32 splits: 1024 warps at batch 16 = one wave)
 
 struct DecodeArgs {
   const __nv_bfloat16 *q;            // [batch][h_q][d]
@@ -435,7 +434,8 @@ __device__ __forceinline__ int visible_block(int idx, int n_init, int ntop, cons
 // ldmatrix), lane 0 the warp's issuer -- the part-B scheme of
 // csrc/sparse_warp.cu.  (16-byte cp.async copies needed ~60 instructions per
 // stage per lane and reached 3.6 TB/s, profiles/r02o.)
-constexpr int kDW = 2;                        // warps per CTA (4 CTAs, 8 warps per SM)
+constexpr int kDW = 4;                        // warps per CTA (2 CTAs per SM)
+constexpr int kDCl = 8;                       // CTAs per cluster = per (sequence, group) row
 constexpr int kDStages = 3;                   // ring depth: 2 stages in flight while one computes
 constexpr int kDStageKeys = 16;
 constexpr uint32_t kDTile = kDStageKeys * kD * 2;  // 4 KB
@@ -469,18 +469,42 @@ struct AttnMaps {
   CUtensorMap k, v;  // page pools as (d lo/hi 64, pool row, half, group): box {64, 16, 2, 1}
 };
 
-__global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a, const int32_t *topk,
-                                                                  const int32_t *topk_cnt,
-                                                                  float *part_o, float2 *part_ml,
-                                                                  int splits,
-                                                                  const __grid_constant__ AttnMaps maps) {
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 ld_cluster_f32x2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(kDCl, 1, 1) __launch_bounds__(kDW * 32)
+    decode_attn_cluster_kernel(DecodeArgs a, const int32_t *topk, const int32_t *topk_cnt,
+                               __nv_bfloat16 *o_out, float *lse_out,
+                               const __grid_constant__ AttnMaps maps) {
   extern __shared__ uint8_t dsm_raw[];
   uint8_t *dsm = dsm_raw + ((1024u - (tc::smem_u32(dsm_raw) & 1023u)) & 1023u);
   auto ring = reinterpret_cast<uint8_t(*)[kDStages][2][kDTile]>(dsm);  // [warp][stage][K|V]
   __shared__ uint64_t full_s[kDW][kDStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = blockIdx.x * kDW + warp;
-  if (unit >= a.batch * a.h_kv * splits) return;
+  const uint32_t crank = cluster_ctarank();   // = blockIdx.x (cluster spans x)
+  const int wid = (int)crank * kDW + warp;    // warp of the row, 0 .. kDCl * kDW - 1
+  const int row = blockIdx.y;
   uint64_t *full = full_s[warp];
   if (lane == 0) {
     for (int k = 0; k < kDStages; ++k) tc::mbar_init(&full[k], 1);
@@ -489,7 +513,6 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
   __syncwarp();
   pdl_launch_dependents();
   pdl_wait();  // top-k (and its re-rank)
-  const int row = unit / splits, split = unit % splits;
   const int seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
   const int64_t i = L - 1;
@@ -501,16 +524,10 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
   // an empty slot (no cached token) has no visible block: no page is read
   const int nvis = L < 1 ? 0 : n_init + ntop + (b + 1 - lo2);
   const int32_t *top = topk + (int64_t)row * a.k_top;
-  const int vb0 = split * kAttnBlocks, vb1 = min(nvis, vb0 + kAttnBlocks);
-  const int64_t pi_base = ((int64_t)row * splits + split) * kG;
+  // the row's visible blocks spread evenly over its kDCl x kDW warps
+  const int per = (nvis + kDCl * kDW - 1) / (kDCl * kDW);
+  const int vb0 = min(nvis, wid * per), vb1 = min(nvis, vb0 + per);
   const int h0 = lane >> 2;
-  if (vb0 >= vb1) {
-    if ((lane & 3) == 0) {
-      part_ml[pi_base + h0] = make_float2(-INFINITY, 0.f);
-      part_ml[pi_base + h0 + 8] = make_float2(-INFINITY, 0.f);
-    }
-    return;
-  }
   // q of the group as A fragments straight from global memory:
   // a0 = (head h0, d k), a1 = (h0 + 8, k), a2 = (h0, k + 8), a3 = (h0 + 8, k + 8)
   const int lm = lane >> 3, lr = lane & 7;
@@ -527,9 +544,9 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
       qa[ks][3] = __ldg(q1 + ks * 8 + 4 + dw);
     }
   }
-  // the warp's <= kAttnBlocks block ids and their pages, looked up once
-  // (lane l holds block vb0 + l): a per-stage topk -> block_table -> page
-  // chain of dependent loads was the kernel's top stall (profiles/r02n)
+  // the warp's <= 32 block ids and their pages, looked up once (lane l holds
+  // block vb0 + l): a per-stage topk -> block_table -> page chain of
+  // dependent loads was the kernel's top stall (profiles/r02n)
   int my_j = 0, my_page = 0;
   if (lane < vb1 - vb0) {
     my_j = visible_block(vb0 + lane, n_init, ntop, top, lo2);
@@ -622,78 +639,62 @@ __global__ void __launch_bounds__(kDW * 32) decode_attn_mma_kernel(DecodeArgs a,
     }
     __syncwarp();  // every lane's reads of this slot are done before it is refilled
   }
-  // partial row sums over the quad, then the partial state of this split
+  // ---- the warp's state -> its (now idle) ring: stats [2][16] then O [16][128] fp32
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  float *st = reinterpret_cast<float *>(ring[warp][0][0]);  // [0,16) m, [16,32) l, [32, ...) O
   const int dc = (lane & 3) * 2;
 #pragma unroll
   for (int jt = 0; jt < 16; ++jt) {
-    *reinterpret_cast<float2 *>(&part_o[(pi_base + h0) * kD + jt * 8 + dc]) = make_float2(o[jt][0], o[jt][1]);
-    *reinterpret_cast<float2 *>(&part_o[(pi_base + h0 + 8) * kD + jt * 8 + dc]) = make_float2(o[jt][2], o[jt][3]);
+    *reinterpret_cast<float2 *>(&st[32 + h0 * kD + jt * 8 + dc]) = make_float2(o[jt][0], o[jt][1]);
+    *reinterpret_cast<float2 *>(&st[32 + (h0 + 8) * kD + jt * 8 + dc]) = make_float2(o[jt][2], o[jt][3]);
   }
   if ((lane & 3) == 0) {
-    part_ml[pi_base + h0] = make_float2(m0, l0);
-    part_ml[pi_base + h0 + 8] = make_float2(m1, l1);
+    st[h0] = m0;
+    st[h0 + 8] = m1;
+    st[16 + h0] = l0;
+    st[16 + h0 + 8] = l1;
   }
-}
-
-// grid (batch*h_kv, 4), 128 threads = 4 heads x 32 lanes (4 d each)
-__global__ void __launch_bounds__(128) decode_combine_kernel(DecodeArgs a, const int32_t *topk_cnt,
-                                                             const float *part_o,
-                                                             const float2 *part_ml, int splits,
-                                                             __nv_bfloat16 *o, float *lse) {
-  const int row = blockIdx.x, seq = row / a.h_kv, g = row % a.h_kv;
-  const int h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  pdl_wait();  // the attention partials
-  const int64_t L = a.seq_lens[seq];
-  if (L < 1) {  // empty slot: defined outputs (O = 0, lse = -inf), nothing read
-    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 0] = __float2bfloat16_rn(0.f);
-    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 1] = __float2bfloat16_rn(0.f);
-    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 2] = __float2bfloat16_rn(0.f);
-    o[((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane + 3] = __float2bfloat16_rn(0.f);
-    if (lane == 0) lse[(int64_t)seq * a.h_q + g * kG + h] = -INFINITY;
-    return;
-  }
-  const int b = (int)((L - 1) / kB);
-  const int n_init = min(a.N_init, b + 1);
-  const int lo2 = max(max(0, b - a.N_local + 1), n_init);
-  const int nvis = n_init + topk_cnt[row] + (b + 1 - lo2);
-  const int used = (int)cdiv(nvis, kAttnBlocks);  // <= 64 splits ((64 + kTopMax) blocks / 3)
-  // lane s holds splits s and s + 32 (<= 64 splits): two loads, warp reductions
-  float2 ml0 = make_float2(-INFINITY, 0.f), ml1 = make_float2(-INFINITY, 0.f);
-  if (lane < used) ml0 = part_ml[((int64_t)row * splits + lane) * kG + h];
-  if (lane + 32 < used) ml1 = part_ml[((int64_t)row * splits + lane + 32) * kG + h];
-  float M = fmaxf(ml0.x, ml1.x);
+  // ---- combine across the cluster through distributed shared memory: CTA
+  // c finalises heads 2c, 2c + 1; thread = (head, 2 d); fixed warp order
+  cluster_sync_all();
+  {
+    const int hh = 2 * (int)crank + (threadIdx.x >> 6), d = (threadIdx.x & 63) * 2;
+    const uint32_t st_local = tc::smem_u32(ring[0][0][0]);
+    constexpr uint32_t kWarpBytes = kDStages * 2 * kDTile;
+    float mv[kDCl * kDW];
+    float M = -INFINITY;
 #pragma unroll
-  for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  const float wl0 = ml0.x == -INFINITY ? 0.f : fast_exp2(ml0.x - M);
-  const float wl1 = ml1.x == -INFINITY ? 0.f : fast_exp2(ml1.x - M);
-  float Ls = ml0.y * wl0 + ml1.y * wl1;
+    for (int w = 0; w < kDCl * kDW; ++w) {
+      const uint32_t ra = mapa_u32(st_local + (w % kDW) * kWarpBytes + hh * 4, w / kDW);
+      mv[w] = ld_cluster_f32(ra);
+      M = fmaxf(M, mv[w]);
+    }
+    float Ls = 0.f, ox = 0.f, oy = 0.f;
 #pragma unroll
-  for (int off = 16; off; off >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, off);
-  // the splits' partial O rows are independent loads (8 in flight)
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-  for (int sp = 0; sp < used; ++sp) {
-    const float w = __shfl_sync(0xffffffffu, sp < 32 ? wl0 : wl1, sp & 31);
-    const int64_t pi = ((int64_t)row * splits + sp) * kG + h;
-    const float4 po = *reinterpret_cast<const float4 *>(&part_o[pi * kD + 4 * lane]);
-    if (w != 0.f) {
-      acc[0] += po.x * w;
-      acc[1] += po.y * w;
-      acc[2] += po.z * w;
-      acc[3] += po.w * w;
+    for (int w = 0; w < kDCl * kDW; ++w) {
+      const uint32_t base = mapa_u32(st_local + (w % kDW) * kWarpBytes, w / kDW);
+      const float wt = mv[w] == -INFINITY ? 0.f : fast_exp2(mv[w] - M);
+      const float lw = ld_cluster_f32(base + (16 + hh) * 4);
+      const float2 ow = ld_cluster_f32x2(base + (32 + hh * kD + d) * 4);
+      Ls += lw * wt;
+      ox += ow.x * wt;
+      oy += ow.y * wt;
+    }
+    if (L >= 1) {
+      const float inv = 1.f / Ls;
+      __nv_bfloat16 *dst = o_out + ((int64_t)seq * a.h_q + g * kG + hh) * kD + d;
+      *reinterpret_cast<__nv_bfloat162 *>(dst) = __floats2bfloat162_rn(ox * inv, oy * inv);
+      if ((threadIdx.x & 63) == 0) lse_out[(int64_t)seq * a.h_q + g * kG + hh] = (M + __log2f(Ls)) * 0.6931471805599453f;
+    } else {  // empty slot: defined outputs (O = 0, lse = -inf), nothing was read
+      __nv_bfloat16 *dst = o_out + ((int64_t)seq * a.h_q + g * kG + hh) * kD + d;
+      *reinterpret_cast<__nv_bfloat162 *>(dst) = __floats2bfloat162_rn(0.f, 0.f);
+      if ((threadIdx.x & 63) == 0) lse_out[(int64_t)seq * a.h_q + g * kG + hh] = -INFINITY;
     }
   }
-  const float inv = 1.f / Ls;
-  __nv_bfloat16 *dst = o + ((int64_t)seq * a.h_q + g * kG + h) * kD + 4 * lane;
-  __align__(8) __nv_bfloat16 ov[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) ov[e] = __float2bfloat16_rn(acc[e] * inv);
-  *reinterpret_cast<uint2 *>(dst) = *reinterpret_cast<const uint2 *>(ov);
-  if (lane == 0) lse[(int64_t)seq * a.h_q + g * kG + h] = (M + __log2f(Ls)) * 0.6931471805599453f;
+  cluster_sync_all();  // peers' shared memory stays valid until every read is done
 }
 
 static DecodeArgs make_args(const swattn_config *cfg, const swattn_paged_kv *kv, const void *q,
@@ -725,9 +726,9 @@ static DecodeArgs make_args(const swattn_config *cfg, const swattn_paged_kv *kv,
 }
 
 struct DecodeLayout {
-  int p1_splits, tiles, attn_splits, max_ctx;
+  int p1_splits, tiles, max_ctx;
   int64_t ld;
-  size_t off_p1, off_scmp, off_flags, off_topk, off_cnt, off_count, off_rows, off_part, off_po, off_pml, total;
+  size_t off_p1, off_scmp, off_flags, off_topk, off_cnt, off_count, off_rows, off_part, total;
 };
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -738,10 +739,8 @@ static DecodeLayout decode_layout(const swattn_config *cfg, int batch, int max_p
   const int64_t m1 = num_pooled(D.max_ctx, cfg->l_C1, cfg->s_C1);
   const int64_t m2 = num_pooled(D.max_ctx, cfg->l_C2, cfg->s_C2);
   const int64_t n_cols = m1 ? cdiv(m1, cfg->s) : 0;
-  static_assert(64 + kTopMax <= 64 * kAttnBlocks, "decode_combine_kernel keeps two splits per lane");
   D.p1_splits = (int)std::max<int64_t>(1, cdiv(std::max(m2, m1), kP1Cols));
   D.tiles = (int)std::max<int64_t>(1, cdiv(n_cols, kTileBlocks));
-  D.attn_splits = (int)cdiv(cfg->N_init + cfg->N_local + cfg->k_top, kAttnBlocks);
   D.ld = ((n_cols + 3) / 4) * 4 + 4;
   const int64_t rows = (int64_t)batch * cfg->h_kv;
   size_t o = 0;
@@ -753,8 +752,6 @@ static DecodeLayout decode_layout(const swattn_config *cfg, int batch, int max_p
   D.off_count = o; o = al(o + 16);
   D.off_rows = o; o = al(o + 2 * rows * sizeof(int32_t));  // row ids + k-th keys
   D.off_part = o; o = al(o + rerank_partials_bytes());
-  D.off_po = o; o = al(o + rows * D.attn_splits * kG * kD * sizeof(float));
-  D.off_pml = o; o = al(o + rows * D.attn_splits * kG * sizeof(float2));
   D.total = o;
   return D;
 }
@@ -841,8 +838,6 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
   int32_t *cnt = reinterpret_cast<int32_t *>(ws + D.off_cnt);
   int32_t *count = reinterpret_cast<int32_t *>(ws + D.off_count);
   int32_t *rows = reinterpret_cast<int32_t *>(ws + D.off_rows);
-  float *po = reinterpret_cast<float *>(ws + D.off_po);
-  float2 *pml = reinterpret_cast<float2 *>(ws + D.off_pml);
   DecodeArgs a = make_args(cfg, kv, q, batch);
   const int nrows = batch * cfg->h_kv;
   {
@@ -873,11 +868,10 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
                                  num_sms_dec(), st)))
     return rc;
   {
-    const int units = nrows * D.attn_splits;
     const int smem = kDW * kDStages * 2 * kDTile + 1024;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(decode_attn_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
     AttnMaps maps;
@@ -893,13 +887,13 @@ int32_t swattn_decode_step(const swattn_config *cfg, const swattn_paged_kv *kv, 
         return SWATTN_ECUDA;
       }
     }
-    launch_pdl(decode_attn_mma_kernel, dim3((units + kDW - 1) / kDW), dim3(kDW * 32), smem, st, a,
-               (const int32_t *)topk, (const int32_t *)cnt, po, pml, D.attn_splits, maps);
-    SWATTN_LAUNCH_CHECK("decode_attn_mma_kernel");
+    // one cluster of kDCl CTAs per (sequence, group) row; the split states
+    // are combined in distributed shared memory (no partial-O round trip
+    // through HBM, no combine kernel)
+    launch_pdl(decode_attn_cluster_kernel, dim3(kDCl, nrows), dim3(kDW * 32), smem, st, a,
+               (const int32_t *)topk, (const int32_t *)cnt, static_cast<__nv_bfloat16 *>(o), lse, maps);
+    SWATTN_LAUNCH_CHECK("decode_attn_cluster_kernel");
   }
-  launch_pdl(decode_combine_kernel, dim3(nrows, kG / 4), dim3(128), 0, st, a, (const int32_t *)cnt,
-             (const float *)po, (const float2 *)pml, D.attn_splits, static_cast<__nv_bfloat16 *>(o), lse);
-  SWATTN_LAUNCH_CHECK("decode_combine_kernel");
   return SWATTN_OK;
 }
 
