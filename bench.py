@@ -208,7 +208,7 @@ def _max_over_ranks(ms, ws):
     import torch.distributed as dist
     if ws <= 1:
         return ms
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ms], device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -259,6 +259,12 @@ def run_ours(args):
     import torch.distributed as dist
 
     ws, rank, local = _dist()
+    # SWATTN_BENCH_SHARE_GPU=1 (test only): every rank on cuda:0 with gloo, to
+    # exercise the N > 1 logic (spawn, barriers, max over ranks, rank-0 line)
+    # on a one-GPU lease; its timings are meaningless
+    share = os.environ.get("SWATTN_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1 or args.cp_sharded:
         if args.cp_sharded and ws == 1:
@@ -266,7 +272,10 @@ def run_ours(args):
             os.environ.setdefault("MASTER_PORT", "29517")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     strong = args.cp or args.cp_sharded
     from paper_2509_24663_b200 import _lib
     from paper_2509_24663_b200.core import AttentionConfig, make_qkv
