@@ -416,13 +416,6 @@ __global__ void __launch_bounds__(128) decode_pass2_kernel(DecodeArgs a, const f
 }
 
 // ------------------------------------------------------------ D5 attention
-__device__ __forceinline__ int visible_block(int idx, int n_init, int ntop, const int32_t *top,
-                                             int lo2) {
-  if (idx < n_init) return idx;
-  idx -= n_init;
-  if (idx < ntop) return top[idx];
-  return lo2 + (idx - ntop);
-}
 
 // ---- D5 on the tensor cores: one warp = (row, split of kAttnBlocks blocks);
 // the row's 16 query heads are the M = 16 of mma.sync.m16n8k16 (as in the
@@ -494,7 +487,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 __global__ void __cluster_dims__(kDCl, 1, 1) __launch_bounds__(kDW * 32)
-    decode_attn_cluster_kernel(DecodeArgs a, const int32_t *topk, const int32_t *topk_cnt,
+    decode_attn_cluster_kernel(DecodeArgs a, const int32_t *topk, const int32_t * /* topk_cnt */,
                                __nv_bfloat16 *o_out, float *lse_out,
                                const __grid_constant__ AttnMaps maps) {
   extern __shared__ uint8_t dsm_raw[];
@@ -512,7 +505,6 @@ __global__ void __cluster_dims__(kDCl, 1, 1) __launch_bounds__(kDW * 32)
   }
   __syncwarp();
   pdl_launch_dependents();
-  pdl_wait();  // top-k (and its re-rank)
   const int seq = row / a.h_kv, g = row % a.h_kv;
   const int64_t L = a.seq_lens[seq];
   const int64_t i = L - 1;
@@ -520,13 +512,22 @@ __global__ void __cluster_dims__(kDCl, 1, 1) __launch_bounds__(kDW * 32)
   const int n_init = min(a.N_init, b + 1);
   const int lo = max(0, b - a.N_local + 1);
   const int lo2 = max(lo, n_init);
-  const int ntop = topk_cnt[row];
+  const int nloc = b + 1 - lo2;
+  // the row's top-k count is a function of its length (topk_cta.cuh), so the
+  // block -> warp map is known before the top-k kernels finish
+  const int64_t m1_row = num_pooled(L, a.l_C1, a.s_C1);
+  const int ncand = max(0, cand_hi(b, a.N_local, (int)(m1_row ? cdiv(m1_row, kPoolS) : 0)) - a.N_init);
+  const int ntop = (L < 1 || i + 1 < a.l_C1) ? 0 : min(ncand, a.k_top);
   // an empty slot (no cached token) has no visible block: no page is read
-  const int nvis = L < 1 ? 0 : n_init + ntop + (b + 1 - lo2);
+  const int nvis = L < 1 ? 0 : n_init + nloc + ntop;
   const int32_t *top = topk + (int64_t)row * a.k_top;
-  // the row's visible blocks spread evenly over its kDCl x kDW warps
+  // visible blocks in the order init, local, top-k, spread evenly over the
+  // row's kDCl x kDW warps: warps holding only init / local blocks (a third
+  // of the row) need nothing from the top-k kernels and start streaming
+  // before the programmatic-launch wait, the others wait for the selection
   const int per = (nvis + kDCl * kDW - 1) / (kDCl * kDW);
   const int vb0 = min(nvis, wid * per), vb1 = min(nvis, vb0 + per);
+  if (vb1 > n_init + nloc) pdl_wait();  // top-k (and its re-rank)
   const int h0 = lane >> 2;
   // q of the group as A fragments straight from global memory:
   // a0 = (head h0, d k), a1 = (h0 + 8, k), a2 = (h0, k + 8), a3 = (h0 + 8, k + 8)
@@ -549,7 +550,8 @@ __global__ void __cluster_dims__(kDCl, 1, 1) __launch_bounds__(kDW * 32)
   // dependent loads was the kernel's top stall (profiles/r02n)
   int my_j = 0, my_page = 0;
   if (lane < vb1 - vb0) {
-    my_j = visible_block(vb0 + lane, n_init, ntop, top, lo2);
+    const int idx = vb0 + lane;
+    my_j = idx < n_init ? idx : idx < n_init + nloc ? lo2 + (idx - n_init) : top[idx - n_init - nloc];
     my_page = a.block_table[(int64_t)seq * a.max_pages + my_j];
   }
   // stage s of this warp's key stream: block vb0 + s / 4, rows (s % 4) * 16 ..
