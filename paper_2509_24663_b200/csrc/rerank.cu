@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "topk_cta.cuh"
 
 namespace swattn {
 
@@ -45,7 +46,8 @@ struct RerankArgs {
 // kP1Split CTAs (rerank_p1_kernel) so a handful of rows -- the decode case --
 // is not serialised on one SM each; larger counts keep one CTA per row.
 constexpr int kSplitRows = 256;
-constexpr int kP1Split = 16;
+constexpr int kP1Split = 64;
+constexpr int kNarrow = 32;  // split path: columns per sub-chunk (thread = (head, column pair))
 
 struct RowInfo {
   int g;
@@ -170,14 +172,72 @@ __device__ void pass1_range(const RerankArgs &a, const __nv_bfloat16 *kc, int g,
   __syncthreads();
 }
 
+// float64 (max, sum) of the 16 heads over columns [c_lo, c_hi) for the split
+// path: sub-chunks of 32 columns staged row-major [c][d] (8 KB), thread =
+// (head t / 16, columns 2 (t % 16), +1), two accumulators per column (even /
+// odd d), then a 16-lane shuffle merge per head.  A quarter of pass1_range's
+// per-thread DFMA chain per 32 columns, so a flagged decode row's pass 1 is
+// spread over 64 short CTAs.  Result in mh[h], lh[h] (log-sum of the slice).
+__device__ void pass1_narrow(const RerankArgs &a, const __nv_bfloat16 *kc, int g, int64_t c_lo,
+                             int64_t c_hi, const double (*q_s)[kG], __nv_bfloat16 *kn,
+                             double *mh, double *lh) {
+  const int h = threadIdx.x >> 4, cp = threadIdx.x & 15;
+  double M = -INFINITY, S = 0.0;
+  for (int64_t c0 = c_lo; c0 < c_hi; c0 += kNarrow) {
+    __syncthreads();
+    for (int v = threadIdx.x; v < kNarrow * (kD / 8); v += kThreads) {
+      const int c = v / (kD / 8), d8 = (v % (kD / 8)) * 8;
+      uint4 raw = make_uint4(0, 0, 0, 0);
+      if (c0 + c < c_hi) raw = __ldg(reinterpret_cast<const uint4 *>(kc + ((c0 + c) * a.h_kv + g) * kD + d8));
+      *reinterpret_cast<uint4 *>(&kn[c * kD + d8]) = raw;
+    }
+    __syncthreads();
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    const uint32_t *k0 = reinterpret_cast<const uint32_t *>(&kn[(2 * cp) * kD]);
+    const uint32_t *k1 = reinterpret_cast<const uint32_t *>(&kn[(2 * cp + 1) * kD]);
+#pragma unroll 8
+    for (int d2 = 0; d2 < kD / 2; ++d2) {
+      const double q0 = q_s[2 * d2][h], q1 = q_s[2 * d2 + 1][h];
+      const uint32_t x = k0[d2], y = k1[d2];
+      a0 = fma(q0, (double)__uint_as_float(x << 16), a0);
+      a1 = fma(q1, (double)__uint_as_float(x & 0xffff0000u), a1);
+      b0 = fma(q0, (double)__uint_as_float(y << 16), b0);
+      b1 = fma(q1, (double)__uint_as_float(y & 0xffff0000u), b1);
+    }
+    const bool v0 = c0 + 2 * cp < c_hi, v1 = c0 + 2 * cp + 1 < c_hi;
+    const double s0 = v0 ? (a0 + a1) * a.scale : -INFINITY, s1 = v1 ? (b0 + b1) * a.scale : -INFINITY;
+    const double m = fmax(fmax(s0, s1), M);
+    if (m != -INFINITY) {
+      S = (M == -INFINITY ? 0.0 : S * exp(M - m)) + (v0 ? exp(s0 - m) : 0.0) + (v1 ? exp(s1 - m) : 0.0);
+      M = m;
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const double oM = __shfl_xor_sync(0xffffffffu, M, o), oS = __shfl_xor_sync(0xffffffffu, S, o);
+    const double m = fmax(M, oM);
+    if (m != -INFINITY) {
+      S = (M == -INFINITY ? 0.0 : S * exp(M - m)) + (oM == -INFINITY ? 0.0 : oS * exp(oM - m));
+      M = m;
+    }
+  }
+  if (cp == 0) {
+    mh[h] = M;
+    lh[h] = S;
+  }
+  __syncthreads();
+}
+
 // pass-1 partials for the row-split path: work item = (flagged row, column slice)
 __global__ void __launch_bounds__(kThreads, 2) rerank_p1_kernel(RerankArgs a) {
   __shared__ __align__(16) double q_s[kD][kG];
   __shared__ double wm[kThreads / 32][4], wl[kThreads / 32][4];
   __shared__ double mh[kG], lh[kG];
   extern __shared__ __nv_bfloat16 kc_s[];  // [kD][kChunk]
-  pdl_launch_dependents();
   pdl_wait();  // flagged rows come from the top-k kernel
+  // dependents (the re-rank kernel) are released only now, so they may read
+  // the top-k outputs before their own wait (which then covers the partials)
+  pdl_launch_dependents();
   const int total = min(*a.count, a.cap);
   if (total > kSplitRows || a.partials == nullptr) return;
   for (int w = blockIdx.x; w < total * kP1Split; w += gridDim.x) {
@@ -186,12 +246,14 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_p1_kernel(RerankArgs a) {
     const __nv_bfloat16 *kc;
     int64_t vis;
     pass1_keys(a, r, kc, vis);
-    const int64_t len = cdiv(cdiv(vis, (int64_t)kP1Split), (int64_t)kChunk) * kChunk;
+    const int64_t len = cdiv(cdiv(vis, (int64_t)kP1Split), (int64_t)kNarrow) * kNarrow;
     const int64_t lo = min((int64_t)part * len, vis), hi = min(lo + len, vis);
     __syncthreads();
     load_q(a, r, q_s);
     __syncthreads();
-    pass1_range(a, kc, r.g, lo, hi, q_s, kc_s, wm, wl, mh, lh);
+    (void)wm;
+    (void)wl;
+    pass1_narrow(a, kc, r.g, lo, hi, q_s, kc_s, mh, lh);
     if (threadIdx.x < kG)
       a.partials[((int64_t)item * kP1Split + part) * kG + threadIdx.x] =
           make_double2(mh[threadIdx.x], lh[threadIdx.x]);
@@ -206,10 +268,14 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
   __shared__ int members[kMaxCluster];
   __shared__ double mscore[kMaxCluster];
   __shared__ int n_members, n_above;
+  __shared__ uint32_t abits[kTopkMaxCand / 32];  // candidates above the band
 
   __shared__ double mh[kG], lh[kG];
   pdl_launch_dependents();
-  pdl_wait();  // flagged rows / pass-1 partials from the preceding kernels
+  // The predecessor (rerank_p1_kernel) releases this grid only after its own
+  // wait, so the top-k outputs (count, rows, S^cmp) are complete here; only
+  // the pass-1 partials need the wait, placed right before they are read --
+  // q staging, the cluster scan and the members' dot products overlap pass 1.
   const int total = min(*a.count, a.cap);
   const bool split = total <= kSplitRows && a.partials != nullptr;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -224,22 +290,98 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
     const int k = min(a.k_top, ncand);
     __syncthreads();
     load_q(a, ri, q_s);
-    __syncthreads();
     const int64_t vis1 = vis_count(i, a.l_C1, a.s_C1);
 
-    // ---- pass 1 in float64: lse over the visible normaliser columns
-    if (split) {
-      if (threadIdx.x < kG) {
-        const int h = threadIdx.x;
-        double M = -INFINITY;
-        for (int pp = 0; pp < kP1Split; ++pp)
-          M = fmax(M, a.partials[((int64_t)item * kP1Split + pp) * kG + h].x);
-        double L = 0.0;
-        for (int pp = 0; pp < kP1Split; ++pp) {
-          const double2 v = a.partials[((int64_t)item * kP1Split + pp) * kG + h];
-          if (v.x != -INFINITY) L += v.y * exp(v.x - M);
+    // ---- the boundary cluster from the float32 scores (complete here, see
+    // above); blocks above the band are marked for the settle step
+    const float *src = a.s_cmp + (int64_t)row * a.ld;
+    // k-th largest float32 score key, recorded by K3 next to the row id
+    const uint32_t T = (uint32_t)a.rows[a.cap + item];
+    const float vk = key2f(T);
+    const float band = 3.0f * kScoreRelErr * fabsf(vk);
+    const int nwords = (ncand + 31) >> 5;
+    if (threadIdx.x == 0) { n_members = 0; n_above = 0; }
+    for (int w = threadIdx.x; w < nwords; w += kThreads) abits[w] = 0u;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ncand; t += kThreads) {
+      const float v = src[a.N_init + t];
+      if (v > vk + band) {
+        atomicAdd(&n_above, 1);
+        atomicOr(&abits[t >> 5], 1u << (t & 31));
+      } else if (v >= vk - band) {
+        const int slot = atomicAdd(&n_members, 1);
+        if (slot < kMaxCluster) members[slot] = a.N_init + t;
+      }
+    }
+    __syncthreads();
+    const int nm = min(n_members, kMaxCluster);
+
+    // ---- float64 max-pooled scores of the cluster members: warp = member,
+    // lane = (head lane & 15, window columns lane >> 4, +2, +4).  The dot
+    // products need no pass-1 statistics, so each warp's first member is
+    // scored before the pass-1 wait; its <= 6 window rows are staged in the
+    // idle staging buffer (one coalesced 16-byte load per lane and row), then
+    // two-accumulator dot products from shared memory
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hh = lane & 15, c_half = lane >> 4;
+    __nv_bfloat16 *wrows = kc_s + warp * 6 * kD;
+    auto member_dots = [&](int j, double (&dot)[3], bool (&inwin)[3]) {
+      for (int v = lane; v < 6 * (kD / 8); v += 32) {
+        const int e = v / (kD / 8), d8 = (v % (kD / 8)) * 8;
+        const int64_t c = (int64_t)j * a.ps + e;
+        uint4 raw = make_uint4(0, 0, 0, 0);
+        if (e < a.pl && c < m1 && c < vis1)
+          raw = __ldg(reinterpret_cast<const uint4 *>(kc1 + (c * a.h_kv + g) * kD + d8));
+        *reinterpret_cast<uint4 *>(&wrows[e * kD + d8]) = raw;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int e = c_half + 2 * q;
+        const int64_t c = (int64_t)j * a.ps + e;
+        inwin[q] = e < a.pl && c < m1;   // window columns past m1 do not exist
+        dot[q] = -INFINITY;              // not visible: contributes nothing (selection.py:212-222)
+        if (inwin[q] && c < vis1) {
+          const uint32_t *kr = reinterpret_cast<const uint32_t *>(&wrows[e * kD]);
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll 8
+          for (int d2 = 0; d2 < kD / 2; ++d2) {
+            const uint32_t kk2 = kr[d2];
+            d0 = fma(q_s[2 * d2][hh], (double)__uint_as_float(kk2 << 16), d0);
+            d1 = fma(q_s[2 * d2 + 1][hh], (double)__uint_as_float(kk2 & 0xffff0000u), d1);
+          }
+          dot[q] = (d0 + d1) * a.scale;
         }
-        lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe (selection.py:204)
+      }
+      __syncwarp();
+    };
+    double dot0[3];
+    bool inw0[3];
+    if (warp < nm) member_dots(members[warp], dot0, inw0);
+
+    // ---- pass 1 in float64: lse over the visible normaliser columns
+    pdl_wait();  // decode: the pass-1 partials of rerank_p1_kernel
+    if (split) {
+      // thread = (head t / 16, partials t % 16 + 16 q): four loads each, then
+      // a 16-lane max / sum (the 64 partials of a flagged row in parallel)
+      {
+        const int h = threadIdx.x >> 4, j = threadIdx.x & 15;
+        double2 v[kP1Split / 16];
+        double M = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < kP1Split / 16; ++q) {
+          v[q] = a.partials[((int64_t)item * kP1Split + j + 16 * q) * kG + h];
+          M = fmax(M, v[q].x);
+        }
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+        double L = 0.0;
+#pragma unroll
+        for (int q = 0; q < kP1Split / 16; ++q)
+          if (v[q].x != -INFINITY) L += v[q].y * exp(v[q].x - M);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        if (j == 0) lse_s[h] = (M == -INFINITY) ? 0.0 : M + log(L);  // lse_safe (selection.py:204)
       }
     } else {
       const __nv_bfloat16 *kc;
@@ -251,53 +393,18 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
     }
     __syncthreads();
 
-    // ---- the boundary cluster from the float32 scores
-    const float *src = a.s_cmp + (int64_t)row * a.ld;
-    // k-th largest float32 score key, recorded by K3 next to the row id
-    const uint32_t T = (uint32_t)a.rows[a.cap + item];
-    const float vk = key2f(T);
-    const float band = 3.0f * kScoreRelErr * fabsf(vk);
-    if (threadIdx.x == 0) { n_members = 0; n_above = 0; }
-    __syncthreads();
-    for (int t = threadIdx.x; t < ncand; t += kThreads) {
-      const float v = src[a.N_init + t];
-      if (v > vk + band) atomicAdd(&n_above, 1);
-      else if (v >= vk - band) {
-        const int slot = atomicAdd(&n_members, 1);
-        if (slot < kMaxCluster) members[slot] = a.N_init + t;
-      }
-    }
-    __syncthreads();
-    const int nm = min(n_members, kMaxCluster);
-
-    // ---- float64 max-pooled scores of the cluster members: warp = member,
-    // lane = (head lane & 15, window columns lane >> 4, +2, +4); each lane
-    // runs its dot products serially over d, heads are summed by shuffles
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int hh = lane & 15, c_half = lane >> 4;
     for (int mi = warp; mi < nm; mi += kThreads / 32) {
-      const int j = members[mi];
-      double val[3];
+      double dot[3];
       bool inwin[3];
+      if (mi == warp) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int e = c_half + 2 * q;
-        const int64_t c = (int64_t)j * a.ps + e;
-        inwin[q] = e < a.pl && c < m1;   // window columns past m1 do not exist
-        double dot = 0.0;
-        if (inwin[q] && c < vis1) {
-          const uint32_t *kr = reinterpret_cast<const uint32_t *>(kc1 + (c * a.h_kv + g) * kD);
-#pragma unroll 8
-          for (int d2 = 0; d2 < kD / 2; ++d2) {
-            const uint32_t kk2 = __ldg(kr + d2);
-            dot = fma(q_s[2 * d2][hh], (double)__uint_as_float(kk2 << 16), dot);
-            dot = fma(q_s[2 * d2 + 1][hh], (double)__uint_as_float(kk2 & 0xffff0000u), dot);
-          }
-          val[q] = exp(dot * a.scale - lse_s[hh]);
-        } else {
-          val[q] = 0.0;  // not visible: contributes nothing (selection.py:212-222)
-        }
+        for (int q = 0; q < 3; ++q) { dot[q] = dot0[q]; inwin[q] = inw0[q]; }
+      } else {
+        member_dots(members[mi], dot, inwin);  // clusters wider than the CTA's warps
       }
+      double val[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) val[q] = dot[q] == -INFINITY ? 0.0 : exp(dot[q] - lse_s[hh]);
 #pragma unroll
       for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -315,13 +422,8 @@ __global__ void __launch_bounds__(kThreads, 2) rerank_kernel(RerankArgs a) {
     // The row's selection is then a bitmap over the candidates (above-cluster
     // blocks + chosen members) in the now idle staging buffer, emitted in
     // ascending order by a block-wide scan of per-thread word counts.
-    uint32_t *bits = reinterpret_cast<uint32_t *>(kc_s);
+    uint32_t *bits = abits;  // above-band blocks from the cluster scan
     int *wsum = reinterpret_cast<int *>(kc_s) + (kChunk * kD / 2 - kThreads);  // tail of kc_s
-    const int nwords = (ncand + 31) >> 5;
-    for (int w = threadIdx.x; w < nwords; w += kThreads) bits[w] = 0u;
-    __syncthreads();
-    for (int t = threadIdx.x; t < ncand; t += kThreads)
-      if (src[a.N_init + t] > vk + band) atomicOr(&bits[t >> 5], 1u << (t & 31));
     if (threadIdx.x == 0) {
       const int slots = k - n_above;
       // selection sort over the (small) cluster
