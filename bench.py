@@ -681,16 +681,20 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        # one process per GPU: re-execute under torch.distributed.run
+        # one process per GPU, as torch.distributed.run would start them (its
+        # argument parser would also claim abbreviations such as --n)
         import socket
         sk = socket.socket()
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
         sk.close()
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
-               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-        sys.exit(subprocess.call(cmd))
+        procs = []
+        for r in range(args.gpus):
+            env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                       LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+            procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                          env=env))
+        sys.exit(max(pr.wait() for pr in procs))
     if args.impl == "reference":
         run_reference(args)
     else:
