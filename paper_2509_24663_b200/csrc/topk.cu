@@ -26,7 +26,8 @@ namespace swattn {
 namespace {
 
 constexpr int kWarps = 8;
-constexpr int kMaxCand = 4096;  // per-row candidate bound held in smem
+constexpr int kMaxCand = kTopkMaxCand;  // per-row candidate bound (8192 blocks: n <= 524K)
+constexpr int kStageCap = 4096;         // candidates a warp stages in shared memory
 
 // Select the k best of ncand candidate scores src[0..ncand) (block ids
 // N_init + t) into out[0..k_top) ascending (-1 padded).  Warp-cooperative.
@@ -192,6 +193,10 @@ __device__ void warp_topk_row(const float *__restrict__ src, int ncand, int k, i
   const int lane = threadIdx.x & 31;
   if (k == ncand) {  // every candidate is selected (or none)
     for (int t = lane; t < k_top; t += 32) out[t] = t < k ? N_init + t : -1;
+    return;
+  }
+  if (ncand > kStageCap) {  // long rows (> 256K tokens): radix select straight from S^cmp
+    warp_topk_generic(GlobalKeys{src}, ncand, k, N_init, k_top, out, hist, amb, row);
     return;
   }
   for (int t = lane; t < ncand; t += 32) ks[t] = f2key(src[t]);
@@ -575,7 +580,7 @@ int32_t launch_topk(const swattn_config *cfg, const float *s_cmp, int64_t ld, in
   const GroupRange gr = group_range(cfg);
   const int64_t rows = (int64_t)gr.gc * (r1 - r0);
   AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
-  const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
+  const int cand_stride = std::min(n_cols > cfg->N_init ? n_cols - cfg->N_init : 1, kStageCap);
   const unsigned grid = (unsigned)cdiv(rows, kWarps);
   if (reg_path_ok(s_cmp, ld, cfg->k_top, n_cols)) {
     topk_kernel<true><<<grid, kWarps * 32, 0, stream>>>(
@@ -604,12 +609,12 @@ int32_t launch_topk_tail(const swattn_config *cfg, const float *s_cmp, int64_t l
   const int64_t tok0 = (int64_t)(cfg->N_init + cfg->N_local) * cfg->B;
   const int64_t t1 = std::min(r1, std::max(tok0, r0));
   AmbList amb{amb_count, amb_rows, amb_cap, flags, ld_f};
-  const int cand_stride = n_cols > cfg->N_init ? n_cols - cfg->N_init : 1;
+  const int cand_stride = std::min(n_cols > cfg->N_init ? n_cols - cfg->N_init : 1, kStageCap);
   const size_t smem = (size_t)kWarps * cand_stride * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(topk_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kWarps * kMaxCand * sizeof(uint32_t)));
+                         (int)(kWarps * kStageCap * sizeof(uint32_t)));
     attr = true;
   }
   topk_tail_kernel<<<148, kWarps * 32, smem, stream>>>(

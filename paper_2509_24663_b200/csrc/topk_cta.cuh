@@ -16,7 +16,7 @@
 
 namespace swattn {
 
-constexpr int kTopkMaxCand = 4096;  // per-row candidate bound (block ids < 4096 + N_init)
+constexpr int kTopkMaxCand = 8192;  // per-row candidate bound (block ids < 8192 + N_init: n <= 524K)
 
 // Outputs of K2 when it selects the top-k in its pass-2 epilogue (row f1):
 // rows whose candidate set overflowed (massive exact ties) are listed for
