@@ -261,6 +261,17 @@ typedef struct swattn_paged_kv {
 int32_t swattn_kcache_append(const swattn_config *cfg, const swattn_paged_kv *kv,
                              const int32_t *prev_lens, int32_t batch, void *stream);
 
+/* Serving-loop append of ONE token per sequence, entirely on the device:
+ * K, V [batch, h_kv, d_h] bf16 are written at position seq_lens[b] (the
+ * block table must already map page seq_lens[b] / B), the compressed keys
+ * are extended, and seq_lens[b] is advanced by one (kv->seq_lens is written
+ * through).  active [batch] int32 (NULL = all): sequences with active[b] == 0
+ * are left untouched.  One launch, no host synchronisation; capturable in a
+ * CUDA graph together with swattn_decode_step. */
+int32_t swattn_kcache_append_tokens(const swattn_config *cfg, const swattn_paged_kv *kv,
+                                    const void *K, const void *V, const int32_t *active,
+                                    int32_t batch, void *stream);
+
 /* One decode step: q [batch, h_q, d_h] bf16 for token seq_lens[b]-1 ->
  * o [batch, h_q, d_h] bf16, lse [batch, h_q] fp32; topk [batch, h_kv, k_top]
  * int32 (optional, may be NULL). */

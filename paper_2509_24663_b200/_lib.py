@@ -99,6 +99,7 @@ def lib():
                                             SZ, P]),
         "swattn_workspace_ckeys": (I32, [cfgp, I64, P, ctypes.POINTER(P), ctypes.POINTER(P)]),
         "swattn_kcache_append": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P]),
+        "swattn_kcache_append_tokens": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, P, P, I32, P]),
         "swattn_decode_step": (I32, [cfgp, ctypes.POINTER(CPagedKV), P, I32, P, P, P, P, SZ, P]),
         "swattn_decode_workspace_bytes": (SZ, [cfgp, I32, I32]),
         "swattn_decode_reranked_offset": (I64, [cfgp, I32, I32]),
@@ -118,7 +119,7 @@ EXPORTED = (
     "swattn_sparse_workspace_bytes", "swattn_sparse_fwd_lists", "swattn_sparse_bwd", "swattn_sparse_bwd_workspace_bytes",
     "swattn_dense_bwd", "swattn_dense_bwd_workspace_bytes",
     "swattn_dense_fwd", "swattn_attend", "swattn_select_blocks_rows", "swattn_sparse_fwd_rows",
-    "swattn_attend_rows", "swattn_attend_prepare", "swattn_attend_groups", "swattn_attend_rows_groups", "swattn_workspace_ckeys", "swattn_kcache_append", "swattn_decode_step",
+    "swattn_attend_rows", "swattn_attend_prepare", "swattn_attend_groups", "swattn_attend_rows_groups", "swattn_workspace_ckeys", "swattn_kcache_append", "swattn_kcache_append_tokens", "swattn_decode_step",
     "swattn_decode_workspace_bytes", "swattn_decode_reranked_offset",
 )
 

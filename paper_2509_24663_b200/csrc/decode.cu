@@ -64,10 +64,10 @@ __device__ __forceinline__ const __nv_bfloat16 *page_row(const __nv_bfloat16 *pa
 }
 
 // ------------------------------------------------------------ D1 append
-// grid (batch, h_kv), 128 threads = d; new windows are few per step.
-__global__ void kcache_append_kernel(DecodeArgs a, const int32_t *prev_lens) {
-  const int seq = blockIdx.x, g = blockIdx.y, d = threadIdx.x;
-  const int64_t L = a.seq_lens[seq], L0 = prev_lens ? prev_lens[seq] : 0;
+// New C1 / C2 entries of one (sequence, group) when it grew from L0 to L
+// tokens: thread d sums element d of each completed window in float64.
+__device__ __forceinline__ void append_windows(const DecodeArgs &a, int seq, int g, int d, int64_t L0,
+                                               int64_t L) {
   for (int which = 0; which < 2; ++which) {
     const int len = which ? a.l_C2 : a.l_C1, str = which ? a.s_C2 : a.s_C1;
     const int max_m = which ? a.max_m2 : a.max_m1;
@@ -82,6 +82,32 @@ __global__ void kcache_append_kernel(DecodeArgs a, const int32_t *prev_lens) {
       dst[(j * a.h_kv + g) * kD + d] = __float2bfloat16_rn(__double2float_rn(s / (double)len));
     }
   }
+}
+
+// grid (batch, h_kv), 128 threads = d; new windows are few per step.
+__global__ void kcache_append_kernel(DecodeArgs a, const int32_t *prev_lens) {
+  const int seq = blockIdx.x, g = blockIdx.y, d = threadIdx.x;
+  append_windows(a, seq, g, d, prev_lens ? prev_lens[seq] : 0, a.seq_lens[seq]);
+}
+
+// One decode token per sequence: grid (batch), h_kv * 128 threads (thread =
+// group x element).  Writes the token's K/V row into its page (the block
+// table already maps page L0 / B), extends the pooled keys, then advances
+// seq_lens[seq] -- after every thread of the CTA has read the old length.
+__global__ void kcache_append_tokens_kernel(DecodeArgs a, const __nv_bfloat16 *K,
+                                            const __nv_bfloat16 *V, const int32_t *active,
+                                            int32_t *seq_lens) {
+  const int seq = blockIdx.x;
+  if (active && !active[seq]) return;
+  const int g = threadIdx.x / kD, d = threadIdx.x % kD;
+  const int64_t L0 = seq_lens[seq];
+  const int64_t src = ((int64_t)seq * a.h_kv + g) * kD + d;
+  const int64_t dst = (page_row(a.k_pages, a.block_table, a.max_pages, seq, L0, a.h_kv, g) - a.k_pages) + d;
+  const_cast<__nv_bfloat16 *>(a.k_pages)[dst] = K[src];
+  const_cast<__nv_bfloat16 *>(a.v_pages)[dst] = V[src];
+  append_windows(a, seq, g, d, L0, L0 + 1);  // reads only rows this thread wrote or older ones
+  __syncthreads();
+  if (threadIdx.x == 0) seq_lens[seq] = (int32_t)(L0 + 1);
 }
 
 // ------------------------------------------------------------ D2 pass 1
@@ -819,6 +845,28 @@ int32_t swattn_kcache_append(const swattn_config *cfg, const swattn_paged_kv *kv
   kcache_append_kernel<<<dim3(batch, cfg->h_kv), kD, 0, static_cast<cudaStream_t>(stream)>>>(
       a, prev_lens);
   SWATTN_LAUNCH_CHECK("kcache_append_kernel");
+  return SWATTN_OK;
+}
+
+int32_t swattn_kcache_append_tokens(const swattn_config *cfg, const swattn_paged_kv *kv,
+                                    const void *K, const void *V, const int32_t *active,
+                                    int32_t batch, void *stream) {
+  int32_t rc = check_decode(cfg, kv, batch);
+  if (rc) return rc;
+  if (!K || !V) {
+    set_error("K and V must be non-null");
+    return SWATTN_EINVAL;
+  }
+  if (cfg->h_kv * kD > 1024) {
+    set_error("h_kv * d_h > 1024 threads per sequence");
+    return SWATTN_EUNSUPPORTED;
+  }
+  if (batch == 0) return SWATTN_OK;
+  DecodeArgs a = make_args(cfg, kv, nullptr, batch);
+  kcache_append_tokens_kernel<<<batch, cfg->h_kv * kD, 0, static_cast<cudaStream_t>(stream)>>>(
+      a, static_cast<const __nv_bfloat16 *>(K), static_cast<const __nv_bfloat16 *>(V), active,
+      const_cast<int32_t *>(kv->seq_lens));
+  SWATTN_LAUNCH_CHECK("kcache_append_tokens_kernel");
   return SWATTN_OK;
 }
 

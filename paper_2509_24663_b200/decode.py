@@ -78,23 +78,57 @@ class PagedKVCache:
 
     def append(self, seq: int, K: torch.Tensor, V: torch.Tensor):
         """Append tokens K/V [n, h_kv, d] to one sequence (prefill or decode),
-        then extend its compressed keys (kernel D1)."""
+        then extend its compressed keys (kernel D1).  Only this sequence's
+        block-table row and length go host -> device."""
         n = K.shape[0]
         L0 = int(self.lens_h[seq])
         self._ensure_pages(seq, L0 + n)
-        self.block_table.copy_(torch.from_numpy(self.block_table_h))
+        self.block_table[seq].copy_(torch.from_numpy(self.block_table_h[seq]))
         pos = torch.arange(L0, L0 + n, device=self.device)
         pages = self.block_table[seq].long()[pos // self.cfg.B]
         slots = pos % self.cfg.B
         self.k_pages[pages, slots] = K.to(torch.bfloat16)
         self.v_pages[pages, slots] = V.to(torch.bfloat16)
-        prev = torch.from_numpy(self.lens_h.copy()).to(self.device)
+        prev = self.seq_lens.clone()
         self.lens_h[seq] = L0 + n
-        self.seq_lens.copy_(torch.from_numpy(self.lens_h))
+        self.seq_lens[seq] = L0 + n
         L = _lib.lib()
         _lib.check(L.swattn_kcache_append(_lib.c_config(self.cfg), self._descriptor(), prev.data_ptr(),
                                           self.batch, _lib.stream_handle(self.device)),
                    "swattn_kcache_append")
+
+    def append_tokens(self, K: torch.Tensor, V: torch.Tensor, active=None):
+        """Serving-loop append: one token per sequence, K/V [batch, h_kv, d].
+        The row write, the pooled-key update and the seq_lens advance run in
+        one kernel (swattn_kcache_append_tokens); the host only uploads the
+        block-table entries of sequences that just crossed into a new page.
+        ``active`` (bool/int [batch], host) masks sequences that do not grow."""
+        cfg = self.cfg
+        if tuple(K.shape) != (self.batch, cfg.h_kv, cfg.d_h) or K.shape != V.shape:
+            raise ValueError(f"K/V shape {tuple(K.shape)}/{tuple(V.shape)} != "
+                             f"{(self.batch, cfg.h_kv, cfg.d_h)}")
+        act = np.ones(self.batch, dtype=bool) if active is None else np.asarray(active, dtype=bool)
+        rows, cols = [], []
+        for b in np.nonzero(act)[0]:
+            L0 = int(self.lens_h[b])
+            if L0 % cfg.B == 0:                       # first token of a new page
+                self._ensure_pages(int(b), L0 + 1)
+                rows.append(int(b)); cols.append(L0 // cfg.B)
+        if rows:
+            r, c = np.array(rows), np.array(cols)
+            vals = torch.from_numpy(self.block_table_h[r, c].copy()).to(self.device, non_blocking=True)
+            self.block_table[torch.from_numpy(r).to(self.device), torch.from_numpy(c).to(self.device)] = vals
+        act_d = None
+        if active is not None:
+            act_d = torch.from_numpy(act.astype(np.int32)).to(self.device)
+        Kd = K.to(torch.bfloat16).contiguous()
+        Vd = V.to(torch.bfloat16).contiguous()
+        self.lens_h += act.astype(np.int32)
+        L = _lib.lib()
+        _lib.check(L.swattn_kcache_append_tokens(_lib.c_config(cfg), self._descriptor(), Kd.data_ptr(),
+                                                 Vd.data_ptr(), 0 if act_d is None else act_d.data_ptr(),
+                                                 self.batch, _lib.stream_handle(self.device)),
+                   "swattn_kcache_append_tokens")
 
 
 def decode_step(cache: PagedKVCache, q: torch.Tensor, return_topk: bool = False):

@@ -339,6 +339,51 @@ def test_decode_incremental_append_equals_bulk():
 
 
 @pytest.mark.gpu
+def test_decode_append_tokens_equals_bulk():
+    """The serving-loop append (one token per sequence per launch, seq_lens
+    advanced on the device, masked sequences left alone) builds the same
+    cache as bulk appends, and decode over it matches the oracle."""
+    from paper_2509_24663_b200.decode import PagedKVCache, decode_step
+    cfg, prof = AttentionConfig(), O.PAPER
+    start, steps = [0, 60, 127, 6000], 70
+    skip = {1: range(10, 20)}                      # sequence 1 idles for ten steps
+    total = [s + steps - len(skip.get(b, ())) for b, s in enumerate(start)]
+    data = [O.draw_qkv(L, 32, 2, 128, 90 + b) for b, L in enumerate(total)]
+    mp = -(-max(total) // 64) + 1
+    a = PagedKVCache(cfg, batch=4, max_pages=mp, seed=3)
+    ref = PagedKVCache(cfg, batch=4, max_pages=mp, seed=4)
+    for b, (Q, K, V) in enumerate(data):
+        ref.append(b, _dev(K), _dev(V))
+        if start[b]:
+            a.append(b, _dev(K[:start[b]]), _dev(V[:start[b]]))
+    pos = list(start)
+    for t in range(steps):
+        act = np.array([t not in skip.get(b, ()) for b in range(4)])
+        Kt = torch.zeros((4, 2, 128), dtype=torch.bfloat16, device="cuda")
+        Vt = torch.zeros_like(Kt)
+        for b in range(4):
+            if act[b]:
+                Kt[b], Vt[b] = _dev(data[b][1][pos[b]]), _dev(data[b][2][pos[b]])
+                pos[b] += 1
+        a.append_tokens(Kt, Vt, active=None if act.all() else act)
+    torch.cuda.synchronize()
+    assert pos == total and a.lens_h.tolist() == total
+    assert a.seq_lens.cpu().tolist() == total
+    assert torch.equal(a.kc1, ref.kc1) and torch.equal(a.kc2, ref.kc2)
+    q = torch.stack([_dev(Q[L - 1]) for (Q, K, V), L in zip(data, total)])
+    ra, ta = decode_step(a, q, return_topk=True)
+    rr, tr = decode_step(ref, q, return_topk=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ta, tr)
+    assert torch.equal(ra.output, rr.output) and torch.equal(ra.lse, rr.lse)
+    for b, ((Q, K, V), L) in enumerate(zip(data, total)):
+        o, l, top = O.decode_row(Q[L - 1], K, V, L - 1, prof)
+        assert np.array_equal(ta[b].cpu().numpy(), top), b
+        err = np.abs(ra.output[b].float().cpu().numpy() - o)
+        assert err.max() <= O_MAX_ABS and err.mean() <= O_MEAN_ABS, (b, err.max())
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name,rows", [("paper_n16384_s2", 4096), ("paper_n10000_s1", 2048)])
 def test_chunked_host_pipeline_equals_whole(name, rows):
     """attend_host_chunked (Q streamed in row chunks, copies overlapped with

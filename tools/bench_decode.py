@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graph", action="store_true",
                     help="capture the step in a CUDA graph and time graph replays")
+    ap.add_argument("--serve", action="store_true",
+                    help="serving-loop step: swattn_kcache_append_tokens (one new token per "
+                         "sequence, seq_lens advanced on the device) + swattn_decode_step")
     args = ap.parse_args()
     cfg = AttentionConfig()
     B, L = args.batch, args.ctx
@@ -53,11 +56,26 @@ def main():
     ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     kv = cache._descriptor()
     stream = torch.cuda.current_stream()
+    if args.serve:
+        # map the pages the timed appends will write (the host-side part of
+        # PagedKVCache.append_tokens), so the device step needs no host work
+        extra = args.warmup + args.steps + 2
+        if (L + extra) > cache.max_pages * cfg.B:
+            raise SystemExit("--serve needs ctx + steps below max_pages * 64")
+        for b in range(B):
+            cache._ensure_pages(b, L + extra)
+        cache.block_table.copy_(torch.from_numpy(cache.block_table_h))
+        knew = torch.randn((B, cfg.h_kv, cfg.d_h), generator=g, device="cuda").to(torch.bfloat16)
+        vnew = torch.randn((B, cfg.h_kv, cfg.d_h), generator=g, device="cuda").to(torch.bfloat16)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    def step():
+    def step(sp=None):
+        sp = sp or stream.cuda_stream
+        if args.serve:
+            _lib.check(Lb.swattn_kcache_append_tokens(c, kv, knew.data_ptr(), vnew.data_ptr(), None, B,
+                                                      sp), "append_tokens")
         _lib.check(Lb.swattn_decode_step(c, kv, q.data_ptr(), B, o.data_ptr(), lse.data_ptr(),
-                                         topk.data_ptr(), ws.data_ptr(), nbytes, stream.cuda_stream),
+                                         topk.data_ptr(), ws.data_ptr(), nbytes, sp),
                    "decode")
 
     for _ in range(args.warmup):
@@ -72,9 +90,7 @@ def main():
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.stream(gs):
             with torch.cuda.graph(graph, stream=gs):
-                _lib.check(Lb.swattn_decode_step(c, kv, q.data_ptr(), B, o.data_ptr(), lse.data_ptr(),
-                                                 topk.data_ptr(), ws.data_ptr(), nbytes,
-                                                 torch.cuda.current_stream().cuda_stream), "decode")
+                step(torch.cuda.current_stream().cuda_stream)
         stream.wait_stream(gs)
         torch.cuda.synchronize()
         run = graph.replay
@@ -135,6 +151,8 @@ def main():
             "higher_is_better": True, "dtype": "bf16", "data": "synthetic (torch.randn K/V/q, seeded)",
             "config": {"workload": f"decode batch {B}, context {L}, paged (64-token pages, shuffled pool)",
                        "launch": "CUDA graph replay" if args.graph else "eager launches",
+                       "step": ("swattn_kcache_append_tokens + swattn_decode_step" if args.serve
+                                else "swattn_decode_step"),
                        "l2": "flushed between steps (256 MB write)"},
             "roofline": {"bound": "hbm", "achieved": bytes_step / (ms / 1e3) / 1e9, "peak": hbm,
                          "unit": "GB/s", "frac": bytes_step / (ms / 1e3) / 1e9 / hbm,

@@ -1,6 +1,5 @@
-#!/bin/bash
-export PYTHONUNBUFFERED=1
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_general.py -m gpu -q -x --timeout 300 > gpurun_out/r02ap_pytest.log 2>&1; echo "parity rc=$?"; tail -1 gpurun_out/r02ap_pytest.log
-timeout 1500 python tools/long_ctx_check.py 262144 393216 524288 557056 > gpurun_out/r02ap_long_ctx.txt 2>&1; echo "long rc=$?"; grep "^n=" gpurun_out/r02ap_long_ctx.txt; tail -3 gpurun_out/r02ap_long_ctx.txt
-timeout 600 python tools/bench_decode.py --ctx 393216 --batch 4 > gpurun_out/r02ap_decode_384k.json 2>&1; echo "decode384k rc=$?"; tail -1 gpurun_out/r02ap_decode_384k.json | cut -c1-250
+set -x
+python -m pytest tests/test_gpu_parity.py -q -x -k "decode" 2>&1 | tail -3
+python tools/bench_decode.py --graph 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('graph', d['ms_per_step'])"
+python tools/bench_decode.py --graph --serve 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('graph+serve', d['ms_per_step'])"
+python tools/bench_decode.py --serve 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('eager+serve', d['ms_per_step'])"
