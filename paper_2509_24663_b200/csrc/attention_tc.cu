@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "route.cuh"
 #include "tc.cuh"
 #include "tma_host.cuh"
 
@@ -52,12 +53,14 @@ struct FaParams {
   int h_q, h_kv, g0, gc;
   int n_tiles;         // token tiles of 8 in this launch
   int tile_end;        // tiles [tile_end - n_tiles, tile_end)
-  int mode;            // 0 dense causal, 1 dense non-causal, 2 sparse part A
+  int mode;            // 0 dense causal, 1 dense non-causal, 2 sparse part A,
+                       // 3 routed tiles (union of the tiles' top-k blocks, route.cuh)
   int N_init, N_local;
   float scale_log2;
   __nv_bfloat16 *O;
   float *lse;          // [n][h_q]
-  float *m_out, *l_out;  // part A: per-row running max (log2) and sum, [n][h_q]
+  float *m_out, *l_out;  // part A: per-row running max (log2) and sum, [n][h_q] (mode 3: in)
+  TileRoutes routes;     // mode 3
 };
 
 struct __align__(1024) FaSmem {
@@ -74,16 +77,28 @@ struct __align__(1024) FaSmem {
 };
 
 // Block list of a tile (query block b): dense 0..b / 0..nb-1, part A init U local.
+// Mode 3: the routed slot's ascending union list.
 struct BlockList {
   int n_first, first_end;  // [0, first_end)
   int second_begin, second_end;  // [second_begin, second_end)
+  const int16_t *ids;      // mode 3
   __device__ int size() const { return first_end + (second_end - second_begin); }
-  __device__ int at(int i) const { return i < first_end ? i : second_begin + (i - first_end); }
+  __device__ int at(int i) const {
+    if (ids != nullptr) return ids[i];
+    return i < first_end ? i : second_begin + (i - first_end);
+  }
 };
 
-__device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t nb_total) {
+template <bool kRouted>
+__device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t nb_total,
+                                               int64_t slot) {
   BlockList L;
-  if (p.mode == 2) {
+  L.ids = nullptr;
+  if (kRouted) {
+    L.first_end = p.routes.ucount[slot];
+    L.second_begin = L.second_end = 0;
+    L.ids = p.routes.ulist + slot * kUCap;
+  } else if (p.mode == 2) {
     const int n_init = min(p.N_init, b + 1);
     const int lo = max(0, b - p.N_local + 1);
     L.first_end = n_init;
@@ -108,12 +123,19 @@ __device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t
 // (o_empty).  TMEM is allocated once per CTA.
 // Persistent CTAs take the items in zig-zag rounds (CTA c gets c, 2G-1-c,
 // 2G+c, ...), so every CTA's heavy-first share sums to about the same work.
-__device__ __forceinline__ int64_t fa_slot_item(int64_t w, int64_t n_items) {
-  const int64_t G = gridDim.x, r = w / G, c = w % G;
+__device__ __forceinline__ int64_t fa_slot_item(int64_t w, int64_t n_items, int64_t G) {
+  const int64_t r = w / G, c = w % G;
   return ((r & 1) && (r + 1) * G <= n_items) ? r * G + (G - 1 - c) : w;
 }
 
+template <bool kRouted>
 __device__ __forceinline__ void fa_item(const FaParams &p, int64_t w, int &tile, int &g) {
+  if (kRouted) {
+    const int32_t it = p.routes.items[w];
+    g = (int)(it / p.routes.ntiles);
+    tile = (int)(it % p.routes.ntiles);
+    return;
+  }
   // group-major (one group's K/V, 67 MB at 128K, stays L2-resident while its
   // tiles run), heavy (late) tiles first within a group
   g = p.g0 + (int)(w / p.n_tiles);
@@ -122,14 +144,23 @@ __device__ __forceinline__ void fa_item(const FaParams &p, int64_t w, int &tile,
 
 // kPersist = false: one item per CTA (the grid covers the items); the item
 // loops below then run once and the running counters fold to constants.
-template <bool kPersist>
+template <bool kPersist, bool kRouted = false>
 __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_constant__ FaParams p) {
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on smem_raw so accesses stay in the shared space
   FaSmem &s = *reinterpret_cast<FaSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nb_total = cdiv(p.n, kBlk);
-  const int64_t n_items = (int64_t)p.n_tiles * p.gc;
+  const int64_t n_items = kRouted ? (int64_t)*p.routes.count : (int64_t)p.n_tiles * p.gc;
+  // routed tiles run beside part B (programmatic launch): the plan's CTA count
+  // works, the rest exit before touching TMEM; the working CTAs wait for part B
+  // at the end so this grid's completion implies part B's.
+  const int64_t ctas = kRouted ? (int64_t)p.routes.plan[0] : (int64_t)gridDim.x;
+  if (kRouted && (int64_t)blockIdx.x >= (ctas > 0 ? ctas : 1)) return;
+  if (kRouted && ctas == 0) {
+    pdl_wait();
+    return;
+  }
 
   if (threadIdx.x == 0) {
     tc::mbar_init(&s.q_full, 1);
@@ -168,22 +199,25 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     }
     uint32_t gi0 = 0;
     int it = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
+    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? ctas : n_items, ++it) {
       int tile, g;
-      fa_item(p, kPersist ? fa_slot_item(w, n_items) : w, tile, g);
+      const int64_t wi = kPersist ? fa_slot_item(w, n_items, ctas) : w;
+      fa_item<kRouted>(p, wi, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
-      const BlockList L = make_list(p, (int)(t0 / kBlk), nb_total);
+      const BlockList L = make_list<kRouted>(p, (int)(t0 / kBlk), nb_total, wi);
       const int nblk = L.size();
       if (lane == 0) {
         if (it > 0) tc::mbar_wait(&s.q_empty, (uint32_t)((it - 1) & 1));
         tc::mbar_arrive_expect_tx(&s.q_full, kQBytes);
         for (int h = 0; h < 2; ++h)
           tc::tma_load_3d(&p.q_map, &s.q_full, s.q + h * (kQBytes / 2), h * 64, g * kG, (int)t0);
+        int nid = L.at(0);
         for (int i = 0; i < nblk; ++i) {
           const uint32_t gi = gi0 + (uint32_t)i;
           const int st = (int)(gi % kStages);
           const uint32_t ph = (((gi / kStages) & 1u) ^ 1u);
-          const int key0 = L.at(i) * kBlk;
+          const int key0 = nid * kBlk;
+          if (i + 1 < nblk) nid = L.at(i + 1);
           tc::mbar_wait(&s.k_empty[st], ph);
           tc::mbar_arrive_expect_tx(&s.k_full[st], kKVBytes);
           for (int h = 0; h < 2; ++h)
@@ -191,11 +225,13 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
                             key0);
         }
       } else if (lane == 1) {
+        int nid = L.at(0);
         for (int i = 0; i < nblk; ++i) {
           const uint32_t gi = gi0 + (uint32_t)i;
           const int st = (int)(gi % kStages);
           const uint32_t ph = (((gi / kStages) & 1u) ^ 1u);
-          const int key0 = L.at(i) * kBlk;
+          const int key0 = nid * kBlk;
+          if (i + 1 < nblk) nid = L.at(i + 1);
           tc::mbar_wait(&s.v_empty[st], ph);
           tc::mbar_arrive_expect_tx(&s.v_full[st], kKVBytes);
           for (int h = 0; h < 2; ++h)
@@ -213,11 +249,12 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     const uint32_t q_addr = tc::smem_u32(s.q);
     uint32_t gi0 = 0;
     int it = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
+    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? ctas : n_items, ++it) {
       int tile, g;
-      fa_item(p, kPersist ? fa_slot_item(w, n_items) : w, tile, g);
+      const int64_t wi = kPersist ? fa_slot_item(w, n_items, ctas) : w;
+      fa_item<kRouted>(p, wi, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
-      const BlockList L = make_list(p, (int)(t0 / kBlk), nb_total);
+      const BlockList L = make_list<kRouted>(p, (int)(t0 / kBlk), nb_total, wi);
       const int nblk = L.size();
       tc::mbar_wait(&s.q_full, (uint32_t)(it & 1));
       tc::tc_fence_after();
@@ -276,17 +313,24 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     uint32_t gi0 = 0;
     int it = 0;
-    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? gridDim.x : n_items, ++it) {
+    for (int64_t w = blockIdx.x; w < n_items; w += kPersist ? ctas : n_items, ++it) {
       int tile, g;
-      fa_item(p, kPersist ? fa_slot_item(w, n_items) : w, tile, g);
+      const int64_t wi = kPersist ? fa_slot_item(w, n_items, ctas) : w;
+      fa_item<kRouted>(p, wi, tile, g);
       const int64_t t0 = (int64_t)tile * kTokTile;
-      const BlockList L = make_list(p, (int)(t0 / kBlk), nb_total);
+      const BlockList L = make_list<kRouted>(p, (int)(t0 / kBlk), nb_total, wi);
       const int nblk = L.size();
       const int64_t tok = t0 + r / kG;
       float m = -INFINITY, l = 0.f;
+      // mode 3: this row's token takes block i of the union iff bit i is set
+      const uint32_t *tbits =
+          kRouted ? p.routes.tbits + (wi * kTokTile + r / kG) * kUWords : nullptr;
+      uint32_t tword = 0;
       for (int i = 0; i < nblk; ++i) {
         const uint32_t gi = gi0 + (uint32_t)i;
-        const int jb = L.at(i);
+        const int jb = kRouted ? 0 : L.at(i);
+        if (kRouted && (i & 31) == 0) tword = tbits[i >> 5];
+        const bool on = !kRouted || ((tword >> (i & 31)) & 1u);
         tc::mbar_wait(&s.s_full[gi & 1u], ((gi >> 1) & 1u));
         tc::tc_fence_after();
         uint32_t ra[32], rb[32];
@@ -297,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         // element) and masking runs only on the diagonal / padded block
         float x[kBlk];
         const int64_t key0 = (int64_t)jb * kBlk;
-        const bool diag = (p.mode != 1) && (key0 + kBlk - 1 > tok);
+        const bool diag = !kRouted && (p.mode != 1) && (key0 + kBlk - 1 > tok);
         const bool pad = (p.mode == 1) && (key0 + kBlk > p.n);
 #pragma unroll
         for (int c = 0; c < kBlk; ++c) x[c] = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
@@ -307,11 +351,11 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
           for (int c = 0; c < kBlk; ++c)
             if (c > lim) x[c] = -INFINITY;
         }
-        const float mx = max64(x) * p.scale_log2;
+        const float mx = on ? max64(x) * p.scale_log2 : -INFINITY;
         // Lazy rescale.  tcgen05.ld / st are warp-collective (.sync.aligned), so
         // the O read-modify-write runs for the whole warp whenever any of its
         // rows needs it; rows that do not scale by 1.
-        const bool want = mx > m + kRescaleThresh || m == -INFINITY;
+        const bool want = on && (mx > m + kRescaleThresh || m == -INFINITY);
         const float m_new = want ? fmaxf(mx, m) : m;
         const bool resc = want && m != -INFINITY && i > 0;
         if (__any_sync(0xffffffffu, resc)) {
@@ -335,12 +379,17 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         m = m_new;
         uint32_t pk[kBlk / 2];
         float rs = 0.f;
+        if (on) {
 #pragma unroll
-        for (int c = 0; c < kBlk; c += 2) {
-          const float p0 = fast_exp2(fmaf(x[c], p.scale_log2, -m));
-          const float p1 = fast_exp2(fmaf(x[c + 1], p.scale_log2, -m));
-          rs += p0 + p1;
-          pk[c / 2] = tc::pack_bf16(p0, p1);
+          for (int c = 0; c < kBlk; c += 2) {
+            const float p0 = fast_exp2(fmaf(x[c], p.scale_log2, -m));
+            const float p1 = fast_exp2(fmaf(x[c + 1], p.scale_log2, -m));
+            rs += p0 + p1;
+            pk[c / 2] = tc::pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
         }
         l += rs;
         tc::tmem_st32(tmem + lane_off + (gi & 1u) * kBlk, pk);
@@ -354,8 +403,23 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       tc::tc_fence_after();
       const bool valid = tok < p.n;
       const int hq = g * kG + (r % kG);
-      const float inv_l = 1.f / l;
-      __nv_bfloat16 *orow = p.O + ((int64_t)tok * p.h_q + hq) * kD;
+      const int64_t idx = tok * p.h_q + hq;
+      float inv_l = 1.f / l;
+      // mode 3: merge with part A (O_A normalised in O, m_A / l_A in m_out /
+      // l_out): O = (O_A l_A 2^(m_A-M) + O_U 2^(m-M)) / (l_A 2^(m_A-M) + l 2^(m-M))
+      float ca = 0.f;
+      if (kRouted && valid) {
+        const float mA = p.m_out[idx], lA = p.l_out[idx];
+        const float M = fmaxf(mA, m);
+        const float wa = lA * fast_exp2(mA - M);
+        const float wu = m == -INFINITY ? 0.f : fast_exp2(m - M);
+        const float den = wa + l * wu;
+        ca = wa / den;
+        inv_l = wu / den;
+        m = M;
+        l = den;
+      }
+      __nv_bfloat16 *orow = p.O + idx * kD;
 #pragma unroll
       for (int c0 = 0; c0 < kD; c0 += 32) {
         uint32_t o[32];
@@ -363,13 +427,30 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         tc::tmem_ld_wait();
         if (valid) {
           uint4 *dst = reinterpret_cast<uint4 *>(orow + c0);
+          if (kRouted) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 8) {
+              const uint4 a = dst[e / 8];
+              const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&aw[q]));
+                o[e + 2 * q] = __float_as_uint(fmaf(f.x, ca, __uint_as_float(o[e + 2 * q]) * inv_l));
+                o[e + 2 * q + 1] =
+                    __float_as_uint(fmaf(f.y, ca, __uint_as_float(o[e + 2 * q + 1]) * inv_l));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * inv_l);
+          }
 #pragma unroll
           for (int e = 0; e < 32; e += 8) {
             uint4 wv;
-            wv.x = tc::pack_bf16(__uint_as_float(o[e]) * inv_l, __uint_as_float(o[e + 1]) * inv_l);
-            wv.y = tc::pack_bf16(__uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l);
-            wv.z = tc::pack_bf16(__uint_as_float(o[e + 4]) * inv_l, __uint_as_float(o[e + 5]) * inv_l);
-            wv.w = tc::pack_bf16(__uint_as_float(o[e + 6]) * inv_l, __uint_as_float(o[e + 7]) * inv_l);
+            wv.x = tc::pack_bf16(__uint_as_float(o[e]), __uint_as_float(o[e + 1]));
+            wv.y = tc::pack_bf16(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+            wv.z = tc::pack_bf16(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5]));
+            wv.w = tc::pack_bf16(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7]));
             dst[e / 8] = wv;
           }
         }
@@ -378,9 +459,8 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       tc::tc_fence_before();
       tc::mbar_arrive(&s.o_empty);
       if (valid) {
-        const int64_t idx = tok * p.h_q + hq;
         p.lse[idx] = (m + __log2f(l)) * 0.6931471805599453f;
-        if (p.m_out != nullptr) {
+        if (p.m_out != nullptr && !kRouted) {
           p.m_out[idx] = m;
           p.l_out[idx] = l;
         }
@@ -391,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem);
+  if (kRouted) pdl_wait();
 }
 
 }  // namespace
@@ -399,7 +480,8 @@ bool attention_tc_available() { return true; }
 
 static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                          int64_t n, int64_t r0, int64_t r1, int mode, void *O, float *lse,
-                         float *m_out, float *l_out, cudaStream_t stream) {
+                         float *m_out, float *l_out, cudaStream_t stream,
+                         const TileRoutes *routes = nullptr) {
   if (r1 <= r0) return SWATTN_OK;
   FaParams p;
   memset(&p, 0, sizeof(p));
@@ -439,11 +521,14 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   p.lse = lse;
   p.m_out = m_out;
   p.l_out = l_out;
+  if (routes != nullptr) p.routes = *routes;
   const size_t smem = sizeof(FaSmem) + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fa_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(fa_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fa_tile_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
   // persistent: two CTAs per SM walk the (tile, group) items
@@ -459,12 +544,20 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   // 4K dense 0.205 -> 0.146 ms, 32K 11.0 -> 8.1 ms); above it one CTA per
   // item lets the block scheduler balance the long causal rows (128K dense:
   // 119 ms one-per-item vs 145 ms persistent).
-  const int64_t items = (int64_t)p.n_tiles * gr.gc;
+  const int64_t items = mode == 3 ? 2 * (int64_t)sms : (int64_t)p.n_tiles * gr.gc;
 #ifndef SWATTN_FA_PERSIST_ITEMS
 #define SWATTN_FA_PERSIST_ITEMS 8192
 #endif
   constexpr int64_t kPersistItems = SWATTN_FA_PERSIST_ITEMS;
-  if (items > kPersistItems) {
+  if (mode == 3) {
+    // programmatic launch behind part B (sparse_warp.cu releases it at once)
+    const cudaError_t e =
+        launch_pdl(fa_tile_kernel<true, true>, dim3((unsigned)items), dim3(kThreads), smem, stream, p);
+    if (e != cudaSuccess) {
+      set_error("fa_tile_kernel (routed) launch: %s", cudaGetErrorString(e));
+      return SWATTN_ECUDA;
+    }
+  } else if (items > kPersistItems) {
     fa_tile_kernel<false><<<(unsigned)items, kThreads, smem, stream>>>(p);
   } else {
     const int64_t grid = items < 2 * (int64_t)sms ? items : 2 * (int64_t)sms;
@@ -477,6 +570,15 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
 int32_t launch_dense_tc(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
   return launch_fa(cfg, Q, K, V, n, 0, n, causal ? 0 : 1, O, lse, nullptr, nullptr, stream);
+}
+
+// Routed tiles (route.cuh): the union of each routed tile's top-k blocks, merged
+// with part A's (O_A, m_A, l_A) into the final O / lse.  The routed count is
+// read on the device: a persistent grid of two CTAs per SM walks the slots.
+int32_t launch_routed_tiles(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                            int64_t n, void *O, float *lse, float *m_a, float *l_a,
+                            const TileRoutes &routes, cudaStream_t stream) {
+  return launch_fa(cfg, Q, K, V, n, 0, n, 3, O, lse, m_a, l_a, stream, &routes);
 }
 
 int32_t launch_sparse_part_a(const swattn_config *cfg, const void *Q, const void *K, const void *V,

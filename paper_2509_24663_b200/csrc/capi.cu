@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "route.cuh"
 #include "topk_cta.cuh"
 
 namespace swattn {
@@ -74,7 +75,12 @@ int32_t launch_sparse_part_b(const swattn_config *, const void *, const void *, 
                              int64_t, int64_t, int64_t, const int32_t *, const int32_t *,
                              const float *,
                              const float *, void *, float *, int32_t *, int32_t *, int,
-                             cudaStream_t);
+                             cudaStream_t, const uint8_t *, const int32_t *);
+int32_t launch_route_plan(const TileRoutes &, int64_t, int, int, cudaStream_t);
+int32_t launch_route_tiles(const swattn_config *, int64_t, int64_t, int64_t, const int32_t *,
+                           const int32_t *, const TileRoutes &, int, cudaStream_t);
+int32_t launch_routed_tiles(const swattn_config *, const void *, const void *, const void *, int64_t,
+                            void *, float *, float *, float *, const TileRoutes &, cudaStream_t);
 int32_t launch_sparse_list(const swattn_config *, const void *, const void *, const void *, int64_t,
                            const int32_t *, int64_t, const int32_t *, void *, float *, int,
                            cudaStream_t);
@@ -111,6 +117,19 @@ static int part_b_ctas() {
     return v > 0 && v < num_sms() ? v : num_sms();
   }();
   return ctas;
+}
+
+// Tile routing threshold (route.cuh): a tile goes to the tensor-core FA tile
+// when |union of its top-k lists| * 100 < sum of the lists * ratio.  On by
+// default up to 48K tokens (8K 1.29 -> 0.77 ms, 16K 3.58 -> 2.47, 32K
+// 7.90 -> 7.30); above it the routed share is small and the FA tile's SMs
+// cost part B about what they save (64K / 128K within noise or slower,
+// profiles/r02aw_route_sweep.txt), so it is off.  SWATTN_ROUTE_PCT overrides
+// (0 disables), read per call.
+static int route_pct(int64_t n) {
+  const char *e = getenv("SWATTN_ROUTE_PCT");
+  if (e) return atoi(e);
+  return n <= 49152 ? 45 : 0;
 }
 
 // The tensor-core kernels are the only path for the paper profile; the
@@ -242,9 +261,9 @@ int64_t swattn_num_pooled(int64_t n, int32_t length, int32_t stride) {
 
 size_t swattn_sparse_workspace_bytes(const swattn_config *cfg, int64_t n) {
   if (cfg == nullptr || n < 1) return 0;
-  // part A row statistics m, l [n][h_q] fp32 + slow-path list
+  // part A row statistics m, l [n][h_q] fp32 + slow-path list + tile routes
   return 2 * align_up((size_t)n * cfg->h_q * 4) + align_up(16) +
-         align_up((size_t)cfg->h_kv * n * 4);
+         align_up((size_t)cfg->h_kv * n * 4) + route_workspace_bytes(cfg->h_kv, n);
 }
 
 size_t swattn_workspace_bytes(const swattn_config *cfg, int64_t n) {
@@ -553,10 +572,23 @@ static int32_t sparse_rows_impl(const swattn_config *cfg, const void *Q, const v
                                                      align_up(16));
     if (!part_a_done && (rc = launch_sparse_part_a(cfg, Q, K, V, n, r0, r1, O, lse, m_a, l_a, st)))
       return rc;
+    const TileRoutes routes = carve_routes(
+        ws + 2 * align_up((size_t)n * cfg->h_q * 4) + align_up(16) + align_up((size_t)cfg->h_kv * n * 4),
+        cfg->h_kv, n);
+    // Routed tiles (route.cuh) run on the SMs part B leaves them, launched
+    // programmatically right behind it; the plan splits the SMs by work.
+    const int pct = route_pct(n);
+    if (pct > 0) {
+      if ((rc = launch_route_tiles(cfg, n, r0, r1, topk, topk_cnt, routes, pct, st))) return rc;
+      if ((rc = launch_route_plan(routes, n, num_sms(), part_b_ctas(), st))) return rc;
+    }
     if ((rc = cuda_check(cudaMemsetAsync(slow_count, 0, 4, st), "memset(slow)"))) return rc;
     rc = launch_sparse_part_b(cfg, Q, K, V, n, r0, r1, topk, topk_cnt, m_a, l_a, O, lse,
-                              slow_count, slow_list, part_b_ctas(), st);
+                              slow_count, slow_list, part_b_ctas(), st,
+                              pct > 0 ? routes.routed : nullptr, pct > 0 ? routes.plan : nullptr);
     if (rc) return rc;
+    if (pct > 0 && (rc = launch_routed_tiles(cfg, Q, K, V, n, O, lse, m_a, l_a, routes, st)))
+      return rc;
     return launch_attention_list(cfg, Q, K, V, n, topk, topk_cnt, slow_count, slow_list, O, lse,
                                  num_sms(), st);
   }

@@ -84,6 +84,9 @@ struct PwParams {
   float *lse;
   float scale_log2;
   int32_t *slow_count, *slow_list;
+  const uint8_t *routed;  // [h_kv][ntiles] tiles finished by the FA tile (route.cuh), or null
+  int64_t ntiles;
+  const int32_t *plan;    // route plan: plan[1] = CTAs that work (the rest exit at once), or null
 };
 
 struct __align__(1024) WarpSmem {
@@ -140,14 +143,15 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
 // Per-warp stream of (token, stage) work: the producer side of the warp's
 // ring.  Lane l holds block ids l and l+32 of the token.
 struct Stream {
-  int64_t it;
+  int64_t it, step;  // step = working CTAs x warps
   int cnt, s, id0, id1, g;
   int64_t t;
   __device__ void load(const PwParams &p, int lane) {
-    for (; it < p.n_items; it += (int64_t)gridDim.x * kWarps) {
+    for (; it < p.n_items; it += step) {
       item_of(p, it, g, t);
       const int64_t row = (int64_t)g * p.n + t;
       cnt = p.topk_cnt[row];
+      if (cnt > 0 && p.routed != nullptr && p.routed[(int64_t)g * p.ntiles + t / 8]) cnt = 0;
       if (cnt > 0) {
         const int32_t *b = p.topk + row * p.k_top;
         id0 = lane < p.k_top ? b[lane] : 0;
@@ -164,7 +168,7 @@ struct Stream {
   }
   __device__ void advance(const PwParams &p, int lane) {
     if (++s == cnt * kStagesPerBlock) {
-      it += (int64_t)gridDim.x * kWarps;
+      it += step;
       load(p, lane);
     }
   }
@@ -174,6 +178,13 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
   extern __shared__ uint8_t smem_raw[];
   PwSmem &sm = *reinterpret_cast<PwSmem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Routed tiles run concurrently on the SMs this launch leaves free: every
+  // CTA releases the dependent (programmatic) launch at once, and the CTAs
+  // beyond the plan's count exit so their SMs take the FA tile's CTAs.
+  pdl_launch_dependents();
+  const int ctas = p.plan != nullptr ? p.plan[1] : (int)gridDim.x;
+  if ((int)blockIdx.x >= ctas) return;
+  const int64_t step = (int64_t)ctas * kWarps;
   WarpSmem &ws = sm.w[warp];
   uint64_t *full = sm.full[warp];
   uint64_t *qfull = &sm.qfull[warp];
@@ -190,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
   // ---- producer cursor: prime the ring and the first Q
   Stream prod;
   prod.it = (int64_t)blockIdx.x * kWarps + warp;
+  prod.step = step;
   prod.load(p, lane);
   if (!prod.valid(p)) return;
   uint32_t issued = 0;  // stages issued (ring position; only its low bits matter)
@@ -224,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
   int64_t qphase = 0;
   Stream cons;
   cons.it = (int64_t)blockIdx.x * kWarps + warp;
+  cons.step = step;
   cons.load(p, lane);
   while (cons.valid(p)) {
     const int64_t row = (int64_t)cons.g * p.n + cons.t;
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
     // next token's Q streams in while this token computes
     {
       Stream nx = cons;
-      nx.it += (int64_t)gridDim.x * kWarps;
+      nx.it += nx.step;
       nx.load(p, lane);
       __syncwarp();
       if (lane == 0 && nx.valid(p)) {
@@ -357,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) sparse_pw_kernel(const __grid_con
       p.lse[ridx + h0] = (mA0 + __log2f(lt0)) * 0.6931471805599453f;
       p.lse[ridx + h0 + 8] = (mA1 + __log2f(lt1)) * 0.6931471805599453f;
     }
-    cons.it += (int64_t)gridDim.x * kWarps;
+    cons.it += cons.step;
     cons.load(p, lane);
   }
 }
@@ -368,7 +381,7 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
                              int64_t n, int64_t r0, int64_t r1, const int32_t *topk, const int32_t *topk_cnt,
                              const float *m_a, const float *l_a, void *O, float *lse,
                              int32_t *slow_count, int32_t *slow_list, int num_sms,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const uint8_t *routed, const int32_t *plan) {
   PwParams p;
   memset(&p, 0, sizeof(p));
   {
@@ -411,6 +424,9 @@ int32_t launch_sparse_part_b(const swattn_config *cfg, const void *Q, const void
   p.scale_log2 = (1.f / sqrtf((float)cfg->d_h)) * 1.4426950408889634f;
   p.slow_count = slow_count;
   p.slow_list = slow_list;
+  p.routed = routed;
+  p.plan = plan;
+  p.ntiles = cdiv(n, 8);
   const size_t smem = sizeof(PwSmem) + 1024;
   static bool attr = false;
   if (!attr) {

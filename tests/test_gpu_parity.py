@@ -242,10 +242,13 @@ def _random_rows(n, k, seed):
     return np.unique(np.concatenate([rng.choice(n, size=k, replace=False), [n - 1, n // 2]]))
 
 
-@pytest.mark.parametrize("n,seed", [(32768, 11), (131072, 12)])
-def test_full_size_properties_and_sampled_rows(n, seed):
+@pytest.mark.parametrize("n,seed,route", [(32768, 11, None), (131072, 12, None), (65536, 13, "60")])
+def test_full_size_properties_and_sampled_rows(n, seed, route, monkeypatch):
     """BASELINE sizes: the oracle checks sampled rows exactly (selection) and
-    within tolerance (attention); size-independent properties cover the rest."""
+    within tolerance (attention); size-independent properties cover the rest.
+    (32K routes tiles to the FA tile by default; 64K forces it, route.cuh.)"""
+    if route is not None:
+        monkeypatch.setenv("SWATTN_ROUTE_PCT", route)
     prof, cfg = O.PAPER, AttentionConfig()
     Q, K, V = O.draw_qkv(n, 32, 2, 128, seed)
     Qd, Kd, Vd = _dev(Q), _dev(K), _dev(V)
@@ -277,6 +280,31 @@ def test_full_size_properties_and_sampled_rows(n, seed):
     r = torch.as_tensor(rows, device="cuda")
     print(n, "sampled-row sparse err", _tol(res.output[r], want_o, res.lse[r], want_l),
           "reranked rows", int(sel.n_reranked))
+
+
+@pytest.mark.parametrize("name", ["paper_n8192_s0", "paper_n16384_s2", "paper_n10000_s1"])
+def test_routed_tiles_match_part_b(name, monkeypatch):
+    """Tiles routed to the tensor-core FA tile (union of the tile's top-k
+    blocks, per-row block mask, merged with part A -- route.cuh) give the same
+    attention as part B's per-token gathers: both within the oracle bars and
+    within 4e-3 of each other, on every sampled row."""
+    rec, prof, cfg, (Q, K, V), (Qd, Kd, Vd) = _load(name)
+    sel = select_blocks(Qd, Kd, cfg, mode="approx")
+    out = {}
+    for pct in ("0", "100"):
+        monkeypatch.setenv("SWATTN_ROUTE_PCT", pct)
+        res = sparse_forward(Qd, Kd, Vd, sel, cfg)
+        torch.cuda.synchronize()
+        out[pct] = (res.output.float(), res.lse)
+    d = (out["0"][0] - out["100"][0]).abs()
+    assert float(d.max()) <= 4e-3 and float(d.mean()) <= 1e-4, (float(d.max()), float(d.mean()))
+    assert float((out["0"][1] - out["100"][1]).abs().max()) <= 1e-4
+    rows = rec["sparse_rows"]
+    top = rec["topk"].astype(np.int64)
+    want_o, want_l = O.sparse_attention(Q, K, V, top, prof, rows=rows)
+    r = torch.as_tensor(rows, device="cuda")
+    res_o, res_l = out["100"]
+    print(name, "routed max/mean/lse err", _tol(res_o[r].to(torch.bfloat16), want_o, res_l[r], want_l))
 
 
 def test_all_rows_dense_and_forced_sparse_n4096():
