@@ -134,32 +134,44 @@ __global__ void __launch_bounds__(kRW * 32) route_tiles_kernel(const int32_t *to
 // pace (128K: 1.93 ns per pick on 148 or 136 CTAs, c_g growing with n).
 __global__ void route_plan_kernel(TileRoutes R, int64_t n, int num_sms, int pb_max, int fa_sms,
                                   int pb_force, int debug) {
-  if (threadIdx.x != 0) return;
-  const double U = (double)R.sums[0], picks = (double)R.sums[1];
-  const double lg = log2(fmax((double)n, 1.0) / 32768.0) * 0.5;
-  const double c_g = 1.73e-9 + 0.20e-9 * fmin(1.0, fmax(0.0, lg));
-  const double tb_act = picks * c_g, tb_sm = picks * 1.73e-9 * 148.0;
-  int best_s = 0;
-  if (U > 0.0) {
-    double best = 1e30;
-    for (int s = 1; s <= num_sms; ++s) {
-      const int pb = min(num_sms - s, pb_max);
-      const double t_fa = 0.39e-3 + U * 0.385e-6 / s;
-      const double t_pb = picks == 0.0 ? 0.0 : (pb <= 0 ? 1e30 : fmax(tb_act, tb_sm / pb));
-      const double t = fmax(t_fa, t_pb);
-      if (t < best) {
-        best = t;
-        best_s = s;
+  // thread s - 1 evaluates S = s FA SMs; one block-wide argmin
+  __shared__ float best_t[256];
+  __shared__ int best_s[256];
+  const int s = threadIdx.x + 1;
+  const float U = (float)R.sums[0], picks = (float)R.sums[1];
+  const float lg = log2f(fmaxf((float)n, 1.f) / 32768.f) * 0.5f;
+  const float c_g = 1.73e-9f + 0.20e-9f * fminf(1.f, fmaxf(0.f, lg));
+  const float tb_act = picks * c_g, tb_sm = picks * 1.73e-9f * 148.f;
+  float t = 1e30f;
+  if (s <= num_sms) {
+    const int pb = min(num_sms - s, pb_max);
+    const float t_fa = 0.39e-3f + U * 0.385e-6f / (float)s;
+    const float t_pb = picks == 0.f ? 0.f : (pb <= 0 ? 1e30f : fmaxf(tb_act, tb_sm / (float)pb));
+    t = fmaxf(t_fa, t_pb);
+  }
+  best_t[threadIdx.x] = t;
+  best_s[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      const float o = best_t[threadIdx.x + w];
+      const int os = best_s[threadIdx.x + w];
+      if (o < best_t[threadIdx.x] || (o == best_t[threadIdx.x] && os < best_s[threadIdx.x])) {
+        best_t[threadIdx.x] = o;
+        best_s[threadIdx.x] = os;
       }
     }
+    __syncthreads();
   }
-  if (fa_sms >= 0 && U > 0.0) best_s = min(fa_sms, num_sms);
-  R.plan[0] = 2 * best_s;
-  R.plan[1] = min(num_sms - best_s, pb_max);
+  if (threadIdx.x != 0) return;
+  int S = U > 0.f ? best_s[0] : 0;
+  if (fa_sms >= 0 && U > 0.f) S = min(fa_sms, num_sms);
+  R.plan[0] = 2 * S;
+  R.plan[1] = min(num_sms - S, pb_max);
   if (pb_force >= 0) R.plan[1] = min(pb_force, pb_max);
   if (debug)
     printf("route plan: %d tiles, union blocks %llu, part-B picks %llu -> FA SMs %d, part-B CTAs %d\n",
-           *R.count, R.sums[0], R.sums[1], best_s, R.plan[1]);
+           *R.count, R.sums[0], R.sums[1], S, R.plan[1]);
 }
 
 }  // namespace
@@ -170,7 +182,7 @@ int32_t launch_route_plan(const TileRoutes &R, int64_t n, int num_sms, int pb_ma
   const char *f = getenv("SWATTN_ROUTE_FA_SMS");
   const char *d = getenv("SWATTN_ROUTE_DEBUG");
   const char *pf = getenv("SWATTN_ROUTE_PB_FORCE");
-  route_plan_kernel<<<1, 32, 0, stream>>>(R, n, num_sms, pb_max, f ? atoi(f) : -1,
+  route_plan_kernel<<<1, 256, 0, stream>>>(R, n, num_sms < 256 ? num_sms : 256, pb_max, f ? atoi(f) : -1,
                                           pf ? atoi(pf) : -1, d ? atoi(d) : 0);
   SWATTN_LAUNCH_CHECK("route_plan_kernel");
   return SWATTN_OK;
