@@ -76,6 +76,51 @@ struct __align__(1024) FaSmem {
   uint32_t tmem_base;
 };
 
+// Packed fp32 pairs (sm_100: one FFMA2 / FADD2 instruction per two lanes' worth)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipe (degree-3 minimax on the rounded-off
+// fraction, 7.7e-5 relative error -- far below the bf16 rounding of P):
+// takes some exps off MUFU, which the softmax otherwise saturates
+// (16 ex2 / clk / SM, profiles/r02ax_mufu_bench.txt).
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23: round to integer
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);           // x - round(x), |f| <= 0.5
+  float2 q = ffma2(make_float2(0.05508868f, 0.05508868f), f, make_float2(0.24260405f, 0.24260405f));
+  q = ffma2(q, f, make_float2(0.6932762f, 0.6932762f));
+  q = ffma2(q, f, make_float2(0.99992895f, 0.99992895f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
+#ifndef SWATTN_FA_POLY
+// every SWATTN_FA_POLY-th column pair's exps on the FMA pipe (0: none).  Off:
+// 1/8, 1/4, 1/3 of the pairs measured 1 %, 10 %, 10 % slower at 128K dense
+// (profiles/r02bc_fa_poly.txt) -- the softmax warp's issue / latency, not
+// the MUFU rate, bounds it.
+#define SWATTN_FA_POLY 0
+#endif
+
 // Block list of a tile (query block b): dense 0..b / 0..nb-1, part A init U local.
 // Mode 3: the routed slot's ascending union list.
 struct BlockList {
@@ -377,25 +422,62 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
           l *= alpha;
         }
         m = m_new;
+        // P first (argument by packed FFMA2, ex2, pack), released to the MMA
+        // warp, and only then the row sum over the kept exps -- off the
+        // S -> P -> PV critical path
         uint32_t pk[kBlk / 2];
-        float rs = 0.f;
-        if (on) {
+        if constexpr (kRouted) {
+          // (routed tiles keep the inline sum: the deferred one spills at 168 registers)
+          float rs = 0.f;
+          if (on) {
+#pragma unroll
+            for (int c = 0; c < kBlk; c += 2) {
+              const float p0 = fast_exp2(fmaf(x[c], p.scale_log2, -m));
+              const float p1 = fast_exp2(fmaf(x[c + 1], p.scale_log2, -m));
+              rs += p0 + p1;
+              pk[c / 2] = tc::pack_bf16(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
+          }
+          l += rs;
+          tc::tmem_st32(tmem + lane_off + (gi & 1u) * kBlk, pk);
+          tc::tmem_st_wait();
+          tc::tc_fence_before();
+          tc::mbar_arrive(&s.p_full[gi & 1u]);
+          continue;
+        }
+        {
+          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m, -m);
 #pragma unroll
           for (int c = 0; c < kBlk; c += 2) {
-            const float p0 = fast_exp2(fmaf(x[c], p.scale_log2, -m));
-            const float p1 = fast_exp2(fmaf(x[c + 1], p.scale_log2, -m));
-            rs += p0 + p1;
-            pk[c / 2] = tc::pack_bf16(p0, p1);
+            const float2 a2 = ffma2(make_float2(x[c], x[c + 1]), sc2, nm2);
+            if (SWATTN_FA_POLY > 0 && (c / 2) % (SWATTN_FA_POLY > 0 ? SWATTN_FA_POLY : 1) ==
+                                          (SWATTN_FA_POLY > 0 ? SWATTN_FA_POLY - 1 : 0)) {
+              const float2 e2 = poly_exp2x2(a2);
+              x[c] = e2.x;
+              x[c + 1] = e2.y;
+            } else {
+              x[c] = fast_exp2(a2.x);
+              x[c + 1] = fast_exp2(a2.y);
+            }
+            pk[c / 2] = tc::pack_bf16(x[c], x[c + 1]);
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
         }
-        l += rs;
         tc::tmem_st32(tmem + lane_off + (gi & 1u) * kBlk, pk);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         tc::mbar_arrive(&s.p_full[gi & 1u]);
+        {
+          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int c = 0; c < kBlk; c += 4) {
+            s0 = fadd2(s0, make_float2(x[c], x[c + 1]));
+            s1 = fadd2(s1, make_float2(x[c + 2], x[c + 3]));
+          }
+          l += (s0.x + s0.y) + (s1.x + s1.y);
+        }
       }
       // epilogue: PV_{nblk-2} and PV_{nblk-1} may both be in flight here, which a
       // parity wait on o_done cannot tell apart -> dedicated per-item barrier
