@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -125,8 +127,11 @@ class _Chunked:
 
 
 def chunk_rows_for(n: int, B: int) -> int:
-    """~16 chunks, each a multiple of the query block and >= 4096 rows."""
-    rows = max(4096, -(-n // 16))
+    """~8 chunks (SWATTN_HOST_CHUNKS), each a multiple of the query block and
+    >= 4096 rows.  At 128K, 8 chunks measured 47.5-47.8 ms end to end vs
+    48.6-49.0 with 6 / 12 / 16 and 51.2 with 24 (profiles/r02bg_host_chunks.txt):
+    fewer row-range calls, while the copies still hide under compute."""
+    rows = max(4096, -(-n // int(os.environ.get("SWATTN_HOST_CHUNKS", "8"))))
     return -(-rows // B) * B
 
 
