@@ -71,7 +71,7 @@ struct __align__(1024) FaSmem {
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2];
-  uint64_t o_done, o_final;
+  uint64_t o_final;
   uint64_t q_empty, o_empty;  // persistent CTAs: Q slot / O accumulator free for the next item
   uint32_t tmem_base;
 };
@@ -161,7 +161,7 @@ __device__ __forceinline__ BlockList make_list(const FaParams &p, int b, int64_t
 // Persistent: a CTA walks the (tile, group) items blockIdx.x, + gridDim.x, ...
 // (heavy tiles first).  Every barrier phase is derived from running counters
 // -- the global block index gi over all items of the CTA (K/V ring, S / P
-// double buffers, o_done) and the item counter it (Q, o_final, q_empty,
+// double buffers) and the item counter it (Q, o_final, q_empty,
 // o_empty) -- which all four roles advance identically.  Q is reloaded once
 // the previous item's last S MMA completed (q_empty); the first PV of an
 // item waits until the softmax warps have read the previous O out of TMEM
@@ -220,7 +220,6 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       tc::mbar_init(&s.s_full[i], 1);
       tc::mbar_init(&s.p_full[i], 128);
     }
-    tc::mbar_init(&s.o_done, 1);
     tc::mbar_init(&s.o_final, 1);
     tc::mbar_init(&s.o_empty, 128);
     tc::fence_barrier_init();
@@ -286,6 +285,15 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       }
       gi0 += (uint32_t)nblk;
     }
+    // drain: observe the ring phases and the Q slot release the MMA warp
+    // signals after the last issue, so no barrier phase completes unwaited
+    // at exit (keeps compute-sanitizer synccheck clean; costs nothing)
+    if (lane == 0 || lane == 1) {
+      uint64_t *ring = lane == 0 ? s.k_empty : s.v_empty;
+      for (uint32_t gd = gi0 > (uint32_t)kStages ? gi0 - kStages : 0u; gd < gi0; ++gd)
+        tc::mbar_wait(&ring[gd % kStages], (gd / kStages) & 1u);
+      if (lane == 0 && it > 0) tc::mbar_wait(&s.q_empty, (uint32_t)((it - 1) & 1));
+    }
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -342,8 +350,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
             for (int kk = 0; kk < kBlk / 16; ++kk)
               tc::mma_ts(tmem_o, a_p + kk * 8, tc::desc_mnmajor(v_addr + kk * 16 * 128, kKVBytes / 2),
                          id_o, (pi > 0 || kk > 0) ? 1u : 0u);
-            tc::mma_commit(&s.v_empty[st]);
-            tc::mma_commit(&s.o_done);
+            tc::mma_commit(&s.v_empty[st]);  // also tells a rescaling softmax PV_pg is done
             if (pi == nblk - 1) tc::mma_commit(&s.o_final);
           }
           __syncwarp();
@@ -351,6 +358,8 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
       }
       gi0 += (uint32_t)nblk;
     }
+    // drain: the last item's O release (no next item waits for it)
+    if (it > 0) tc::mbar_wait(&s.o_empty, (uint32_t)((it - 1) & 1));
   } else {
     // ------------------------------------------------------------ softmax
     const int quad = warp & 3;
@@ -404,11 +413,11 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         const float m_new = want ? fmaxf(mx, m) : m;
         const bool resc = want && m != -INFINITY && i > 0;
         if (__any_sync(0xffffffffu, resc)) {
-          // S_gi completing implies PV_{gi-2} completed (issue order), so
-          // o_done has 0 or 1 pending phase: the parity wait for completion
-          // #gi (PV_{gi-1}) is unambiguous.
+          // PV_{gi-1} is complete when its V stage is released (v_empty is
+          // committed right after it); that stage's next phase needs P_{gi+1}
+          // from this warp, so the parity wait is unambiguous.
           const float alpha = resc ? fast_exp2(m - m_new) : 1.f;
-          tc::mbar_wait(&s.o_done, ((gi - 1u) & 1u));
+          tc::mbar_wait(&s.v_empty[(gi - 1u) % kStages], ((gi - 1u) / kStages) & 1u);
           tc::tc_fence_after();
 #pragma unroll
           for (int c0 = 0; c0 < kD; c0 += 32) {
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 2) fa_tile_kernel(const __grid_const
         }
       }
       // epilogue: PV_{nblk-2} and PV_{nblk-1} may both be in flight here, which a
-      // parity wait on o_done cannot tell apart -> dedicated per-item barrier
+      // parity wait on one V stage cannot tell apart -> dedicated per-item barrier
       tc::mbar_wait(&s.o_final, (uint32_t)(it & 1));
       tc::tc_fence_after();
       const bool valid = tok < p.n;

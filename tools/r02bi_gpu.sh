@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+for tool in synccheck racecheck memcheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/one_attend.py 8192 > gpurun_out/r02bi_sanitizer_${tool}_attend8192.log 2>&1; echo "attend $tool rc=$?"; tail -2 gpurun_out/r02bi_sanitizer_${tool}_attend8192.log
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/decode_once.py > gpurun_out/r02bi_sanitizer_${tool}_decode.log 2>&1; echo "decode $tool rc=$?"; tail -2 gpurun_out/r02bi_sanitizer_${tool}_decode.log
+done
+timeout 300 python tools/fa_time.py
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
