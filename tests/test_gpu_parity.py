@@ -584,3 +584,74 @@ def test_part_b_overflow_slow_path():
     want_o, want_l = O.sparse_attention(Q, K, V, top, prof, rows=rows)
     r = torch.as_tensor(rows, device="cuda")
     _tol(res.output[r], want_o, res.lse[r], want_l)
+
+
+@pytest.mark.gpu
+def test_decode_serving_loop_cuda_graph():
+    """One serving step -- swattn_kcache_append_tokens (device-side seq_lens
+    advance) + swattn_decode_step -- captured once in a CUDA graph and
+    replayed step after step gives the eager loop's outputs bit for bit
+    (pages mapped ahead by the host, as PagedKVCache.append_tokens does)."""
+    from paper_2509_24663_b200.decode import PagedKVCache
+    cfg, steps, B = AttentionConfig(), 6, 3
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    prompt = [3000, 640, 1]
+    ctx = [torch.randn((L, 2, 128), generator=gen, device="cuda").to(torch.bfloat16) for L in prompt]
+    new_k = torch.randn((steps, B, 2, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    new_v = torch.randn_like(new_k)
+    qs = torch.randn((steps, B, 32, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    L = _lib.lib()
+    c = _lib.c_config(cfg)
+
+    def make():
+        cache = PagedKVCache(cfg, batch=B, max_pages=60, seed=2)
+        for b, K in enumerate(ctx):
+            cache.append(b, K, K.flip(0))
+        for b in range(B):
+            cache._ensure_pages(b, prompt[b] + steps)
+        cache.block_table.copy_(torch.from_numpy(cache.block_table_h))
+        nbytes = L.swattn_decode_workspace_bytes(c, B, cache.max_pages)
+        return cache, torch.empty(nbytes, dtype=torch.uint8, device="cuda"), nbytes
+
+    def step(cache, ws, nbytes, k, v, q, o, lse, topk, stream):
+        kv = cache._descriptor()
+        _lib.check(L.swattn_kcache_append_tokens(c, kv, k.data_ptr(), v.data_ptr(), None, B, stream),
+                   "append_tokens")
+        _lib.check(L.swattn_decode_step(c, kv, q.data_ptr(), B, o.data_ptr(), lse.data_ptr(),
+                                        topk.data_ptr(), ws.data_ptr(), nbytes, stream), "decode")
+
+    # eager loop
+    cache, ws, nbytes = make()
+    st = torch.cuda.current_stream().cuda_stream
+    eager = []
+    for t in range(steps):
+        o = torch.empty((B, 32, 128), dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty((B, 32), dtype=torch.float32, device="cuda")
+        topk = torch.empty((B, 2, cfg.k_top), dtype=torch.int32, device="cuda")
+        step(cache, ws, nbytes, new_k[t], new_v[t], qs[t], o, lse, topk, st)
+        eager.append((o, lse, topk))
+    torch.cuda.synchronize()
+    assert cache.seq_lens.cpu().tolist() == [L0 + steps for L0 in prompt]
+    # graph: static inputs / outputs, one warm-up step eagerly on the capture stream
+    cache, ws, nbytes = make()
+    k_in, v_in, q_in = new_k[0].clone(), new_v[0].clone(), qs[0].clone()
+    o = torch.empty((B, 32, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((B, 32), dtype=torch.float32, device="cuda")
+    topk = torch.empty((B, 2, cfg.k_top), dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(cache, ws, nbytes, k_in, v_in, q_in, o, lse, topk, s.cuda_stream)   # = eager step 0
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            step(cache, ws, nbytes, k_in, v_in, q_in, o, lse, topk, s.cuda_stream)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    assert torch.equal(o, eager[0][0]) and torch.equal(topk, eager[0][2])
+    for t in range(1, steps):
+        k_in.copy_(new_k[t]); v_in.copy_(new_v[t]); q_in.copy_(qs[t])
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(topk, eager[t][2]), t
+        assert torch.equal(o, eager[t][0]) and torch.equal(lse, eager[t][1]), t
+    assert cache.seq_lens.cpu().tolist() == [L0 + steps for L0 in prompt]
