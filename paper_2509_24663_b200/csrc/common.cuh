@@ -110,6 +110,27 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // ex2.approx's 2 ulp), then add n to the exponent field.  x is clamped to
 // [-126, 127]: results below 2^-126 are returned as 2^-126 instead of 0,
 // which only matters for sums in which every term is below 1e-38.
+// Packed fp32 pairs (sm_100a FFMA2 / FADD2: two IEEE fp32 fma / add in one
+// instruction -- bit-identical to two scalar ones, half the issue slots)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 __device__ __forceinline__ float poly_exp2(float x) {
   x = fminf(fmaxf(x, -126.f), 127.f);
   const float t = x + 12582912.f;
