@@ -24,6 +24,7 @@
 //               O / l -> bf16, lse.
 // Roofline: tensor-bound; algorithmic FLOP = 4 * visible_pairs * d_h * h_q
 // (dense.py:167-169 counts x 2).
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -638,8 +639,13 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
   return SWATTN_OK;
 }
 
+int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream);
+
 int32_t launch_dense_tc(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
+  const char *e = getenv("SWATTN_FA2");
+  if (e && atoi(e) == 1) return launch_dense_tc2(cfg, Q, K, V, n, causal, O, lse, stream);
   return launch_fa(cfg, Q, K, V, n, 0, n, causal ? 0 : 1, O, lse, nullptr, nullptr, stream);
 }
 
