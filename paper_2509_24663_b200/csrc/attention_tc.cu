@@ -640,12 +640,18 @@ static int32_t launch_fa(const swattn_config *cfg, const void *Q, const void *K,
 }
 
 int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream);
+                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream, int step);
 
 int32_t launch_dense_tc(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
+  // Causal: the two-tile kernel (attention_tc2.cu) -- 0.82-0.97x the one-tile
+  // time from 2K to 128K (equal at 16K), profiles/r02bn_fa2_ab.txt.
+  // SWATTN_FA2 (per call): 0 one-tile, 1 two-tile, 2 two-tile with 128-key
+  // steps (measurement; slower: its single S buffer serialises each tile).
   const char *e = getenv("SWATTN_FA2");
-  if (e && atoi(e) == 1) return launch_dense_tc2(cfg, Q, K, V, n, causal, O, lse, stream);
+  const int v = e ? atoi(e) : (causal ? 1 : 0);
+  if (v == 1 || v == 2)
+    return launch_dense_tc2(cfg, Q, K, V, n, causal, O, lse, stream, v == 2 ? 128 : 64);
   return launch_fa(cfg, Q, K, V, n, 0, n, causal ? 0 : 1, O, lse, nullptr, nullptr, stream);
 }
 

@@ -22,12 +22,19 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kTokTile = kRows / kG;  // 8 tokens per tile
-constexpr int kBlk = 64;
-constexpr int kStages = 3;
 constexpr int kThreads = 352;
 constexpr uint32_t kQBytes = kRows * kD * 2;  // 32 KB per tile
-constexpr uint32_t kKVBytes = kBlk * kD * 2;  // 16 KB
 constexpr float kRescaleThresh = 8.0f;
+
+// kStep keys per pipeline step: 64 (S double-buffered per tile, 3 K/V
+// stages) or 128 (N = 128 S MMAs -- half the tcgen05.mma issues per key --
+// single S buffer per tile, 2 K/V stages of 32 KB).
+template <int kStep>
+struct StepCfg {
+  static constexpr int kStages = kStep == 64 ? 3 : 2;
+  static constexpr int kSBuf = kStep == 64 ? 2 : 1;
+  static constexpr uint32_t kKVBytes = kStep * kD * 2;
+};
 
 struct Fa2Params {
   CUtensorMap q_map;  // Q [n][h_q][d]: box {64, 16, 8}
@@ -42,10 +49,12 @@ struct Fa2Params {
   float *lse;
 };
 
+template <int kStep>
 struct __align__(1024) Fa2Smem {
+  static constexpr int kStages = StepCfg<kStep>::kStages;
   uint8_t q[2][kQBytes];
-  uint8_t k[kStages][kKVBytes];
-  uint8_t v[kStages][kKVBytes];
+  uint8_t k[kStages][StepCfg<kStep>::kKVBytes];
+  uint8_t v[kStages][StepCfg<kStep>::kKVBytes];
   uint64_t q_full;
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
@@ -54,9 +63,15 @@ struct __align__(1024) Fa2Smem {
   uint32_t tmem_base;
 };
 
+template <int kStep>
 __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_constant__ Fa2Params p) {
+  constexpr int kBlk = kStep;
+  constexpr int kStages = StepCfg<kStep>::kStages;
+  constexpr int kSBuf = StepCfg<kStep>::kSBuf;
+  constexpr uint32_t kKVBytes = StepCfg<kStep>::kKVBytes;
   extern __shared__ uint8_t smem_raw[];
-  Fa2Smem &s = *reinterpret_cast<Fa2Smem *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
+  Fa2Smem<kStep> &s =
+      *reinterpret_cast<Fa2Smem<kStep> *>(smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heavy (late) pairs first, group-major within a wave
   const int w = blockIdx.x;
@@ -64,8 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
   const int pair = p.n_pairs - 1 - w % p.n_pairs;
   const int64_t t0 = (int64_t)pair * 2 * kTokTile;
   const int64_t nb_total = cdiv(p.n, kBlk);
-  const int b = (int)(t0 / kBlk);
-  const int nblk = p.causal ? b + 1 : (int)nb_total;
+  const int nblk = p.causal ? (int)(t0 / kBlk) + 1 : (int)nb_total;  // steps of kStep keys
 
   if (threadIdx.x == 0) {
     tc::mbar_init(&s.q_full, 1);
@@ -76,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
       tc::mbar_init(&s.v_empty[i], 2);
     }
     for (int t = 0; t < 2; ++t)
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < kSBuf; ++i) {
         tc::mbar_init(&s.s_full[t][i], 1);
         tc::mbar_init(&s.p_full[t][i], 128);
       }
@@ -138,43 +152,53 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
     const uint32_t q_addr = tc::smem_u32(s.q[t]);
     tc::mbar_wait(&s.q_full, 0);
     tc::tc_fence_after();
-    for (int i = 0; i <= nblk; ++i) {
-      if (i < nblk) {
-        const int st = i % kStages;
-        tc::mbar_wait(&s.k_full[st], (i / kStages) & 1);
-        tc::tc_fence_after();
-        if (tc::elect_one()) {
-          const uint32_t k_addr = tc::smem_u32(s.k[st]);
-          const uint32_t d_s = tmem + t * 128 + (i & 1) * kBlk;
+    auto issue_s = [&](int i) {
+      const int st = i % kStages;
+      tc::mbar_wait(&s.k_full[st], (i / kStages) & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t k_addr = tc::smem_u32(s.k[st]);
+        const uint32_t d_s = tmem + t * 128 + (i % kSBuf) * 64;
 #pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const int h = kk >> 2, j = kk & 3;
-            tc::mma_ss(d_s, tc::desc_kmajor(q_addr + h * (kQBytes / 2) + j * 32),
-                       tc::desc_kmajor(k_addr + h * (kKVBytes / 2) + j * 32), id_s, kk > 0);
-          }
-          tc::mma_commit(&s.s_full[t][i & 1]);
-          tc::mma_commit(&s.k_empty[st]);
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const int h = kk >> 2, j = kk & 3;
+          tc::mma_ss(d_s, tc::desc_kmajor(q_addr + h * (kQBytes / 2) + j * 32),
+                     tc::desc_kmajor(k_addr + h * (kKVBytes / 2) + j * 32), id_s, kk > 0);
         }
-        __syncwarp();
+        tc::mma_commit(&s.s_full[t][i % kSBuf]);
+        tc::mma_commit(&s.k_empty[st]);
       }
-      if (i >= 1) {
-        const int j = i - 1;
-        const int st = j % kStages;
-        tc::mbar_wait(&s.v_full[st], (j / kStages) & 1);
-        tc::mbar_wait(&s.p_full[t][j & 1], (j >> 1) & 1);
-        tc::tc_fence_after();
-        if (tc::elect_one()) {
-          const uint32_t v_addr = tc::smem_u32(s.v[st]);
-          const uint32_t a_p = tmem + t * 128 + (j & 1) * kBlk;
+      __syncwarp();
+    };
+    auto issue_pv = [&](int j) {
+      const int st = j % kStages;
+      tc::mbar_wait(&s.v_full[st], (j / kStages) & 1);
+      tc::mbar_wait(&s.p_full[t][j % kSBuf], (j / kSBuf) & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t v_addr = tc::smem_u32(s.v[st]);
+        const uint32_t a_p = tmem + t * 128 + (j % kSBuf) * 64;
 #pragma unroll
-          for (int kk = 0; kk < kBlk / 16; ++kk)
-            tc::mma_ts(tmem + 256 + t * 128, a_p + kk * 8,
-                       tc::desc_mnmajor(v_addr + kk * 16 * 128, kKVBytes / 2), id_o,
-                       (j > 0 || kk > 0) ? 1u : 0u);
-          tc::mma_commit(&s.v_empty[st]);
-          if (j == nblk - 1) tc::mma_commit(&s.o_final[t]);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < kBlk / 16; ++kk)
+          tc::mma_ts(tmem + 256 + t * 128, a_p + kk * 8,
+                     tc::desc_mnmajor(v_addr + kk * 16 * 128, kKVBytes / 2), id_o,
+                     (j > 0 || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&s.v_empty[st]);
+        if (j == nblk - 1) tc::mma_commit(&s.o_final[t]);
+      }
+      __syncwarp();
+    };
+    // double-buffered S: S(i) goes out while the softmax still works on
+    // S(i-1), then PV(i-1); single-buffered S (128-key steps): PV(i-1) must
+    // consume P(i-1) before S(i) overwrites it -- the tile's own pipeline is
+    // serial and the other tile's issuer fills the tensor pipe meanwhile
+    for (int i = 0; i <= nblk; ++i) {
+      if (kSBuf == 2) {
+        if (i < nblk) issue_s(i);
+        if (i >= 1) issue_pv(i - 1);
+      } else {
+        if (i >= 1) issue_pv(i - 1);
+        if (i < nblk) issue_s(i);
       }
     }
   } else {
@@ -187,25 +211,38 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
     const int64_t tok = t0 + tile * kTokTile + r / kG;
     float m = -INFINITY, l = 0.f;
     for (int i = 0; i < nblk; ++i) {
-      tc::mbar_wait(&s.s_full[tile][i & 1], (i >> 1) & 1);
+      tc::mbar_wait(&s.s_full[tile][i % kSBuf], (i / kSBuf) & 1);
       tc::tc_fence_after();
-      uint32_t ra[32], rb[32];
-      tc::tmem_ld32(tmem_s + lane_off + (i & 1) * kBlk, ra);
-      tc::tmem_ld32(tmem_s + lane_off + (i & 1) * kBlk + 32, rb);
-      tc::tmem_ld_wait();
-      float x[kBlk];
+      const uint32_t sbuf = tmem_s + lane_off + (i % kSBuf) * 64;
       const int64_t key0 = (int64_t)i * kBlk;
       const bool diag = p.causal && (key0 + kBlk - 1 > tok);
       const bool pad = !p.causal && (key0 + kBlk > p.n);
+      const int64_t lim = diag ? tok - key0 : p.n - 1 - key0;  // last visible column (diag / pad)
+      // 64 columns of S (chunk c0) with the diagonal / padding mask
+      auto load64 = [&](int c0, float (&x)[64]) {
+        uint32_t ra[32], rb[32];
+        tc::tmem_ld32(sbuf + c0, ra);
+        tc::tmem_ld32(sbuf + c0 + 32, rb);
+        tc::tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < kBlk; ++c) x[c] = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
-      if (diag || pad) {
-        const int64_t lim = diag ? tok - key0 : p.n - 1 - key0;
+        for (int c = 0; c < 64; ++c) x[c] = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
+        if (diag || pad) {
 #pragma unroll
-        for (int c = 0; c < kBlk; ++c)
-          if (c > lim) x[c] = -INFINITY;
+          for (int c = 0; c < 64; ++c)
+            if (c0 + c > lim) x[c] = -INFINITY;
+        }
+      };
+      float x[64];
+      load64(0, x);
+      float mx = max64(x);
+      if constexpr (kBlk == 128) {
+        // pass 1 of 2 over TMEM: the second chunk's max only (x keeps chunk 0
+        // for nothing -- it is reloaded in pass 2 to bound the registers)
+        float y[64];
+        load64(64, y);
+        mx = fmaxf(mx, max64(y));
       }
-      const float mx = max64(x) * p.scale_log2;
+      mx *= p.scale_log2;
       const bool want = mx > m + kRescaleThresh || m == -INFINITY;
       const float m_new = want ? fmaxf(mx, m) : m;
       const bool resc = want && m != -INFINITY && i > 0;
@@ -228,28 +265,57 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
         l *= alpha;
       }
       m = m_new;
-      uint32_t pk[kBlk / 2];
-      {
+      if constexpr (kBlk == 64) {
+        // P first, released to the MMA warp, then the row sum off the critical path
+        uint32_t pk[32];
         const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m, -m);
 #pragma unroll
-        for (int c = 0; c < kBlk; c += 2) {
+        for (int c = 0; c < 64; c += 2) {
           const float2 a2 = ffma2(make_float2(x[c], x[c + 1]), sc2, nm2);
           x[c] = fast_exp2(a2.x);
           x[c + 1] = fast_exp2(a2.y);
           pk[c / 2] = tc::pack_bf16(x[c], x[c + 1]);
         }
-      }
-      tc::tmem_st32(tmem_s + lane_off + (i & 1) * kBlk, pk);
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&s.p_full[tile][i & 1]);
-      float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+        tc::tmem_st32(sbuf, pk);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&s.p_full[tile][i % kSBuf]);
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < kBlk; c += 4) {
-        s0 = fadd2(s0, make_float2(x[c], x[c + 1]));
-        s1 = fadd2(s1, make_float2(x[c + 2], x[c + 3]));
+        for (int c = 0; c < 64; c += 4) {
+          s0 = fadd2(s0, make_float2(x[c], x[c + 1]));
+          s1 = fadd2(s1, make_float2(x[c + 2], x[c + 3]));
+        }
+        l += (s0.x + s0.y) + (s1.x + s1.y);
+      } else {
+        // pass 2: both chunks reloaded, exps packed; P overwrites S columns
+        // 0..63, so it is stored only after both chunks are read
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m, -m);
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+        uint32_t pw0[32], pw1[32];
+        auto exps = [&](const float (&xx)[64], uint32_t (&pw)[32]) {
+#pragma unroll
+          for (int c = 0; c < 64; c += 4) {
+            const float2 a01 = ffma2(make_float2(xx[c], xx[c + 1]), sc2, nm2);
+            const float2 a23 = ffma2(make_float2(xx[c + 2], xx[c + 3]), sc2, nm2);
+            const float2 e01 = make_float2(fast_exp2(a01.x), fast_exp2(a01.y));
+            const float2 e23 = make_float2(fast_exp2(a23.x), fast_exp2(a23.y));
+            pw[c / 2] = tc::pack_bf16(e01.x, e01.y);
+            pw[c / 2 + 1] = tc::pack_bf16(e23.x, e23.y);
+            s0 = fadd2(s0, e01);
+            s1 = fadd2(s1, e23);
+          }
+        };
+        exps(x, pw0);  // chunk 0 is still in x
+        load64(64, x);
+        exps(x, pw1);
+        tc::tmem_st32(sbuf, pw0);
+        tc::tmem_st32(sbuf + 32, pw1);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&s.p_full[tile][i % kSBuf]);
+        l += (s0.x + s0.y) + (s1.x + s1.y);
       }
-      l += (s0.x + s0.y) + (s1.x + s1.y);
     }
     tc::mbar_wait(&s.o_final[tile], 0);
     tc::tc_fence_after();
@@ -288,8 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
 // Dense causal / non-causal attention of all n rows with two query tiles per
 // CTA (requires n to be a multiple of 16 tokens; the caller falls back to the
 // one-tile kernel otherwise).
-int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
+template <int kStep>
+static int32_t launch_fa2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                          int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
   Fa2Params p;
   memset(&p, 0, sizeof(p));
   {
@@ -304,7 +371,7 @@ int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K,
   {
     const uint64_t dims[2] = {(uint64_t)cfg->h_kv * kD, (uint64_t)n};
     const uint64_t str[1] = {(uint64_t)cfg->h_kv * kD * 2};
-    const uint32_t box[2] = {64, (uint32_t)kBlk};
+    const uint32_t box[2] = {64, (uint32_t)kStep};
     if (!make_tmap_bf16(&p.k_map, K, 2, dims, str, box) ||
         !make_tmap_bf16(&p.v_map, V, 2, dims, str, box)) {
       set_error("cuTensorMapEncodeTiled(K/V) failed");
@@ -322,15 +389,24 @@ int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K,
   p.scale_log2 = (1.f / sqrtf((float)cfg->d_h)) * 1.4426950408889634f;
   p.O = static_cast<__nv_bfloat16 *>(O);
   p.lse = lse;
-  const size_t smem = sizeof(Fa2Smem) + 1024;
+  const size_t smem = sizeof(Fa2Smem<kStep>) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fa2_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fa2_dense_kernel<kStep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
-  fa2_dense_kernel<<<(unsigned)((int64_t)p.n_pairs * gr.gc), kThreads, smem, stream>>>(p);
+  fa2_dense_kernel<kStep><<<(unsigned)((int64_t)p.n_pairs * gr.gc), kThreads, smem, stream>>>(p);
   SWATTN_LAUNCH_CHECK("fa2_dense_kernel");
   return SWATTN_OK;
+}
+
+// Dense causal / non-causal attention of all n rows with two query tiles per
+// CTA; step = 64 or 128 keys per pipeline step.
+int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                         int64_t n, int causal, void *O, float *lse, cudaStream_t stream, int step) {
+  if (step == 128) return launch_fa2<128>(cfg, Q, K, V, n, causal, O, lse, stream);
+  return launch_fa2<64>(cfg, Q, K, V, n, causal, O, lse, stream);
 }
 
 }  // namespace swattn
