@@ -664,9 +664,17 @@ int32_t launch_routed_tiles(const swattn_config *cfg, const void *Q, const void 
   return launch_fa(cfg, Q, K, V, n, 0, n, 3, O, lse, m_a, l_a, stream, &routes);
 }
 
+int32_t launch_part_a_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                          int64_t n, int64_t r0, int64_t r1, void *O, float *lse, float *m_out,
+                          float *l_out, cudaStream_t stream);
+
 int32_t launch_sparse_part_a(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                              int64_t n, int64_t r0, int64_t r1, void *O, float *lse, float *m_out,
                              float *l_out, cudaStream_t stream) {
+  // SWATTN_FA2_PARTA=1 (measurement): part A on the two-tile kernel
+  const char *e = getenv("SWATTN_FA2_PARTA");
+  if (e && atoi(e) == 1 && r0 % 16 == 0)
+    return launch_part_a_tc2(cfg, Q, K, V, n, r0, r1, O, lse, m_out, l_out, stream);
   return launch_fa(cfg, Q, K, V, n, r0, r1, 2, O, lse, m_out, l_out, stream);
 }
 

@@ -42,8 +42,12 @@ struct Fa2Params {
   CUtensorMap v_map;
   int64_t n;
   int h_q, h_kv, g0, gc;
-  int n_pairs;  // 16-token tile pairs
+  int n_pairs;  // 16-token tile pairs of this launch
   int causal;
+  int part_a;    // sparse part A (sparse.py:43-98): init U local blocks only
+  int N_init, N_local;
+  int64_t r0, r1;  // rows [r0, r1) of this launch (r0 a multiple of 16)
+  float *m_out, *l_out;  // part A: per-row running max (log2) and sum
   float scale_log2;
   __nv_bfloat16 *O;
   float *lse;
@@ -77,9 +81,19 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
   const int w = blockIdx.x;
   const int g = p.g0 + w / p.n_pairs;
   const int pair = p.n_pairs - 1 - w % p.n_pairs;
-  const int64_t t0 = (int64_t)pair * 2 * kTokTile;
+  const int64_t t0 = p.r0 + (int64_t)pair * 2 * kTokTile;
   const int64_t nb_total = cdiv(p.n, kBlk);
-  const int nblk = p.causal ? (int)(t0 / kBlk) + 1 : (int)nb_total;  // steps of kStep keys
+  // block list: dense 0..b (causal) / all; part A [0, n_init) U [second, b]
+  const int b = (int)(t0 / kBlk);
+  int nblk, n_init = 0, second = 0;
+  if (p.part_a) {
+    n_init = min(p.N_init, b + 1);
+    second = max(max(0, b - p.N_local + 1), n_init);
+    nblk = n_init + (b + 1 - second);
+  } else {
+    nblk = p.causal ? b + 1 : (int)nb_total;  // steps of kStep keys
+  }
+  auto blk_at = [&](int i) { return p.part_a ? (i < n_init ? i : second + (i - n_init)) : i; };
 
   if (threadIdx.x == 0) {
     tc::mbar_init(&s.q_full, 1);
@@ -121,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
         tc::mbar_arrive_expect_tx(&s.k_full[st], kKVBytes);
         for (int h = 0; h < 2; ++h)
           tc::tma_load_2d(&p.k_map, &s.k_full[st], s.k[st] + h * (kKVBytes / 2), g * kD + h * 64,
-                          i * kBlk);
+                          blk_at(i) * kBlk);
       }
     } else if (lane == 1) {
       tc::tma_prefetch(&p.v_map);
@@ -131,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
         tc::mbar_arrive_expect_tx(&s.v_full[st], kKVBytes);
         for (int h = 0; h < 2; ++h)
           tc::tma_load_2d(&p.v_map, &s.v_full[st], s.v[st] + h * (kKVBytes / 2), g * kD + h * 64,
-                          i * kBlk);
+                          blk_at(i) * kBlk);
       }
     }
     // drain: observe the last ring phases the MMA warp releases
@@ -214,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
       tc::mbar_wait(&s.s_full[tile][i % kSBuf], (i / kSBuf) & 1);
       tc::tc_fence_after();
       const uint32_t sbuf = tmem_s + lane_off + (i % kSBuf) * 64;
-      const int64_t key0 = (int64_t)i * kBlk;
+      const int64_t key0 = (int64_t)blk_at(i) * kBlk;
       const bool diag = p.causal && (key0 + kBlk - 1 > tok);
       const bool pad = !p.causal && (key0 + kBlk > p.n);
       const int64_t lim = diag ? tok - key0 : p.n - 1 - key0;  // last visible column (diag / pad)
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
     }
     tc::mbar_wait(&s.o_final[tile], 0);
     tc::tc_fence_after();
-    const bool valid = tok < p.n;
+    const bool valid = tok < p.r1;
     const int hq = g * kG + (r % kG);
     const int64_t idx = tok * p.h_q + hq;
     const float inv_l = 1.f / l;
@@ -342,7 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
         }
       }
     }
-    if (valid) p.lse[idx] = (m + __log2f(l)) * 0.6931471805599453f;
+    if (valid) {
+      p.lse[idx] = (m + __log2f(l)) * 0.6931471805599453f;
+      if (p.m_out != nullptr) {
+        p.m_out[idx] = m;
+        p.l_out[idx] = l;
+      }
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -356,7 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
 // one-tile kernel otherwise).
 template <int kStep>
 static int32_t launch_fa2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
-                          int64_t n, int causal, void *O, float *lse, cudaStream_t stream) {
+                          int64_t n, int64_t r0, int64_t r1, int causal, int part_a, void *O,
+                          float *lse, float *m_out, float *l_out, cudaStream_t stream) {
+  if (r1 <= r0) return SWATTN_OK;
   Fa2Params p;
   memset(&p, 0, sizeof(p));
   {
@@ -384,8 +406,15 @@ static int32_t launch_fa2(const swattn_config *cfg, const void *Q, const void *K
   const GroupRange gr = group_range(cfg);
   p.g0 = gr.g0;
   p.gc = gr.gc;
-  p.n_pairs = (int)cdiv(n, 2 * kTokTile);
+  p.n_pairs = (int)cdiv(r1 - r0, 2 * kTokTile);
   p.causal = causal;
+  p.part_a = part_a;
+  p.N_init = cfg->N_init;
+  p.N_local = cfg->N_local;
+  p.r0 = r0;
+  p.r1 = r1;
+  p.m_out = m_out;
+  p.l_out = l_out;
   p.scale_log2 = (1.f / sqrtf((float)cfg->d_h)) * 1.4426950408889634f;
   p.O = static_cast<__nv_bfloat16 *>(O);
   p.lse = lse;
@@ -405,8 +434,16 @@ static int32_t launch_fa2(const swattn_config *cfg, const void *Q, const void *K
 // CTA; step = 64 or 128 keys per pipeline step.
 int32_t launch_dense_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
                          int64_t n, int causal, void *O, float *lse, cudaStream_t stream, int step) {
-  if (step == 128) return launch_fa2<128>(cfg, Q, K, V, n, causal, O, lse, stream);
-  return launch_fa2<64>(cfg, Q, K, V, n, causal, O, lse, stream);
+  if (step == 128)
+    return launch_fa2<128>(cfg, Q, K, V, n, 0, n, causal, 0, O, lse, nullptr, nullptr, stream);
+  return launch_fa2<64>(cfg, Q, K, V, n, 0, n, causal, 0, O, lse, nullptr, nullptr, stream);
+}
+
+// Sparse part A of rows [r0, r1) (r0 a multiple of 16) on the two-tile kernel.
+int32_t launch_part_a_tc2(const swattn_config *cfg, const void *Q, const void *K, const void *V,
+                          int64_t n, int64_t r0, int64_t r1, void *O, float *lse, float *m_out,
+                          float *l_out, cudaStream_t stream) {
+  return launch_fa2<64>(cfg, Q, K, V, n, r0, r1, 1, 1, O, lse, m_out, l_out, stream);
 }
 
 }  // namespace swattn
