@@ -53,6 +53,24 @@ struct Fa2Params {
   float *lse;
 };
 
+#ifndef SWATTN_FA2_POLY
+#define SWATTN_FA2_POLY 0  // every Nth column pair's exp2 on the FMA pipe (measurement)
+#endif
+// 2^x for a pair on the FMA pipe: degree-3 minimax on the rounded-off
+// fraction (7.7e-5 relative, below the bf16 rounding of P)
+__device__ __forceinline__ float2 poly_exp2x2_fa2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);
+  float2 q = ffma2(make_float2(0.05508868f, 0.05508868f), f, make_float2(0.24260405f, 0.24260405f));
+  q = ffma2(q, f, make_float2(0.6932762f, 0.6932762f));
+  q = ffma2(q, f, make_float2(0.99992895f, 0.99992895f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
 template <int kStep>
 struct __align__(1024) Fa2Smem {
   static constexpr int kStages = StepCfg<kStep>::kStages;
@@ -286,8 +304,17 @@ __global__ void __launch_bounds__(kThreads, 1) fa2_dense_kernel(const __grid_con
 #pragma unroll
         for (int c = 0; c < 64; c += 2) {
           const float2 a2 = ffma2(make_float2(x[c], x[c + 1]), sc2, nm2);
-          x[c] = fast_exp2(a2.x);
-          x[c + 1] = fast_exp2(a2.y);
+#if SWATTN_FA2_POLY > 0
+          if ((c / 2) % SWATTN_FA2_POLY == SWATTN_FA2_POLY - 1) {
+            const float2 e2 = poly_exp2x2_fa2(a2);
+            x[c] = e2.x;
+            x[c + 1] = e2.y;
+          } else
+#endif
+          {
+            x[c] = fast_exp2(a2.x);
+            x[c + 1] = fast_exp2(a2.y);
+          }
           pk[c / 2] = tc::pack_bf16(x[c], x[c + 1]);
         }
         tc::tmem_st32(sbuf, pk);
