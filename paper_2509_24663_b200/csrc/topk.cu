@@ -253,10 +253,12 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
     return;
   }
   const int lo = N_init, hi = N_init + ncand;  // candidate block ids [lo, hi)
+  // chunks of 128 ids that hold candidates (the rest would only load zeros)
+  const int nch = min(kRegChunks, (hi + 127) / 128);
   // ---- 1. per-lane top-2 (two independent chains over even / odd chunks)
   uint32_t a1 = 0, a2 = 0, b1 = 0, b2 = 0;
-#pragma unroll
-  for (int j = 0; j < kRegChunks; j += 2) {
+#pragma unroll 2
+  for (int j = 0; j < nch; j += 2) {
     uint32_t x[4], y[4];
     load_chunk(row_src, ld, lo, hi, j, lane, x);
     load_chunk(row_src, ld, lo, hi, j + 1, lane, y);
@@ -273,7 +275,7 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
   // ---- 2. survivors
   int mine = 0;
 #pragma unroll 1
-  for (int j = 0; j < kRegChunks; ++j) {
+  for (int j = 0; j < nch; ++j) {
     uint32_t x[4];
     load_chunk(row_src, ld, lo, hi, j, lane, x);
 #pragma unroll
@@ -292,7 +294,7 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
   }
   int pos = incl - mine;
 #pragma unroll 1
-  for (int j = 0; j < kRegChunks; ++j) {
+  for (int j = 0; j < nch; ++j) {
     uint32_t x[4];
     load_chunk(row_src, ld, lo, hi, j, lane, x);
 #pragma unroll
@@ -387,7 +389,7 @@ __device__ void warp_topk_row_reg(const float *__restrict__ row_src, int ld, int
   above = __reduce_min_sync(0xffffffffu, above);
   if (__reduce_max_sync(0xffffffffu, below) == 0u) {
 #pragma unroll 1
-    for (int j = 0; j < kRegChunks; ++j) {
+    for (int j = 0; j < nch; ++j) {
       uint32_t x[4];
       load_chunk(row_src, ld, lo, hi, j, lane, x);
 #pragma unroll
