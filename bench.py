@@ -254,6 +254,31 @@ def count_launches(step):
     return len(names), len(ours), sorted(set(ours))
 
 
+def _bind_to_gpu_numa(dev):
+    """Run this process on the host CPUs local to GPU `dev` (sysfs
+    local_cpulist of its PCI function), so the pinned host buffers of the e2e
+    measurement are first touched -- and placed -- on the GPU's NUMA node:
+    host<->device copies from the far node of a two-socket host run at a
+    fraction of the link rate.  Returns the CPU list used, or None."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return spec
+    except Exception:  # no sysfs entry / no permission: leave the affinity alone
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -340,6 +365,7 @@ def run_ours(args):
         del Q0, K0, V0
 
     # ---- e2e through the public API with host buffers (H2D + D2H in the timed region)
+    numa = _bind_to_gpu_numa(torch.cuda.current_device())
     Qh = Q.cpu().pin_memory()
     Kh = K.cpu().pin_memory()
     Vh = V.cpu().pin_memory()
@@ -443,7 +469,8 @@ def run_ours(args):
                     / (stages["K4_part_B_est"] / 1e3) / 1e12},
             },
             "e2e": {"value": (n if strong else ws * n) / (e2e_ms / 1e3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "host_cpus": numa},
             # counted from the CUPTI trace of one step (count_launches) x steps
             "gpu_launches": (ours_k * args.steps) if ours_k is not None else None,
             "launches_per_step": {"ours": ours_k, "all": total_k, "kernels": our_names},
