@@ -655,3 +655,21 @@ def test_decode_serving_loop_cuda_graph():
         assert torch.equal(topk, eager[t][2]), t
         assert torch.equal(o, eager[t][0]) and torch.equal(lse, eager[t][1]), t
     assert cache.seq_lens.cpu().tolist() == [L0 + steps for L0 in prompt]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [300, 1000, 4100, 6144])
+def test_dense_two_tile_matches_one_tile(n, monkeypatch):
+    """The dense causal default (two query tiles per CTA, attention_tc2.cu)
+    equals the one-tile FA kernel bit for bit, including a partial last tile
+    pair (n % 16 != 0) -- both are checked against the oracle elsewhere."""
+    from paper_2509_24663_b200.core import make_qkv
+    cfg = AttentionConfig()
+    Q, K, V = make_qkv(n, 32, 2, 128, seed=9)
+    out = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("SWATTN_FA2", v)
+        res = tiled_gqa_forward(Q, K, V, cfg)
+        torch.cuda.synchronize()
+        out[v] = (res.output.clone(), res.lse.clone())
+    assert torch.equal(out["0"][0], out["1"][0]) and torch.equal(out["0"][1], out["1"][1])
