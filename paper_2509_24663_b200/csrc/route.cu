@@ -141,7 +141,9 @@ __global__ void route_plan_kernel(TileRoutes R, int64_t n, int num_sms, int pb_m
   const float U = (float)R.sums[0], picks = (float)R.sums[1];
   const float lg = log2f(fmaxf((float)n, 1.f) / 32768.f) * 0.5f;
   const float c_g = 1.73e-9f + 0.20e-9f * fminf(1.f, fmaxf(0.f, lg));
-  const float tb_act = picks * c_g, tb_sm = picks * 1.73e-9f * 148.f;
+  // per-pick costs were measured chip-wide on 148 SMs: scale to this GPU's count
+  const float chip = 148.f / (float)num_sms;
+  const float tb_act = picks * c_g * chip, tb_sm = picks * 1.73e-9f * 148.f;
   float t = 1e30f;
   if (s <= num_sms) {
     const int pb = min(num_sms - s, pb_max);
